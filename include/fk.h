@@ -1,0 +1,145 @@
+/*
+ * fk.h — C-ABI of the B200 partial-assembly (PA) operator library
+ * (libfk_b200.so, built from paper_2603_09038_b200/csrc).
+ *
+ * This is the drop-in boundary for the hot path the reference package
+ * feklab composes on the CPU (/root/reference/pkg/src/feklab):
+ *
+ *   gather (mesh.py:130-131) -> B/G contractions (tensor.py:220-283)
+ *   -> pointwise PA data D (operator.py:132-193) -> B^T/G^T contractions
+ *   -> scatter_add (mesh.py:133-137)
+ *
+ * fused into one sm_100a kernel per operator (BP1 mass / BP3 diffusion) and
+ * order p = 1..8, plus the Jacobi-PCG solve that calls it and the z-slab
+ * interface exchange for multi-GPU runs.  Plain pointers and sizes only; no
+ * torch types.  Device pointers are FP64, contiguous, on the handle's device.
+ *
+ * Errors: every call returns FK_OK (0) or a negative code; the message of the
+ * last failing call on this thread is fk_last_error().  A handle is not
+ * thread-safe; all work is enqueued on the handle's stream and calls return
+ * without synchronising unless stated.
+ */
+#ifndef FK_B200_H
+#define FK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FK_API_VERSION 1
+
+#define FK_OK 0
+#define FK_EINVAL (-1)      /* invalid argument / shape ("... do not match ...") */
+#define FK_ECUDA (-2)       /* CUDA runtime error */
+#define FK_ENCCL (-3)       /* NCCL error */
+#define FK_ENOMEM (-4)      /* device allocation failed */
+#define FK_EUNSUPPORTED (-5) /* order / quadrature / variant not compiled */
+
+/* Operator kinds (CEED bake-off problems). */
+#define FK_KIND_MASS 1      /* BP1: y = G^T B^T W|J| B G x                      */
+#define FK_KIND_DIFFUSION 3 /* BP3: y = G^T (B,G)^T W|J| J^-1 J^-T (B,G) G x     */
+
+/* Kernel variants for the element contractions. */
+#define FK_VARIANT_AUTO 0   /* per-order choice from the measured sweep */
+#define FK_VARIANT_DFMA 1   /* register-blocked FP64 FMA, basis in the constant bank */
+#define FK_VARIANT_DMMA 2   /* warp mma.sync.m8n8k4 f64 tiles (DMMA.8x8x4)           */
+
+typedef struct fk_op fk_op;
+typedef struct fk_comm fk_comm;
+
+typedef struct fk_op_desc {
+  int kind;           /* FK_KIND_MASS | FK_KIND_DIFFUSION */
+  int p;              /* polynomial order 1..8 (d = p+1 GLL nodes per direction) */
+  int q;              /* Gauss points per direction: p+1 or p+2 */
+  int nx, ny;         /* elements along x, y (mesh.py:78) */
+  int nz_local;       /* element layers owned by this rank (z-slab) */
+  int z0_layer;       /* first global element layer owned by this rank */
+  int nz_global;      /* global element layers */
+  double jac_diag[3]; /* constant Jacobian diagonal h/2 (Mesh.jacobian_diag, mesh.py:56-60) */
+  double jac_det;     /* Mesh.jacobian_det (mesh.py:62-64) */
+  const double* B;    /* host, q*d row-major: B[a*d+i] = L_i(x_a) (Basis1D.values, tensor.py:77-119) */
+  const double* G;    /* host, q*d row-major: Basis1D.gradients */
+  const double* w;    /* host, q Gauss weights: Basis1D.quad_weights */
+  const int64_t* gather_ids; /* optional host map (nel_local, d^3) of GLOBAL ids as
+                                h1_restriction().gather_ids rows (mesh.py:144-166);
+                                NULL => built on device from the closed form */
+  int dirichlet;      /* 1: homogeneous essential BC on the six box faces
+                         (constrained operator, diagonal one) */
+  int variant;        /* FK_VARIANT_* */
+  int device;         /* CUDA ordinal */
+  void* stream;       /* cudaStream_t (NULL: the legacy default stream) */
+  fk_comm* comm;      /* NULL for one rank; else the z-slab communicator */
+} fk_op_desc;
+
+typedef struct fk_op_info {
+  int64_t ndof_local;  /* L-vector length on this rank: npx*npy*(nz_local*p+1) */
+  int64_t nel_local;   /* nx*ny*nz_local */
+  int64_t dof_offset;  /* global id of local dof 0: z0_layer*p*npx*npy */
+  int64_t ndof_global; /* npx*npy*npz */
+  int64_t pa_bytes;    /* bytes of stored PA data D on the device */
+  int variant;         /* variant actually used by fk_op_apply */
+  int elems_per_block; /* launch geometry of the fused kernel */
+  int threads_per_block;
+  int blocks;          /* persistent grid size */
+} fk_op_info;
+
+int fk_version(void);
+const char* fk_last_error(void);
+
+/* Lifecycle.  fk_op_create validates the descriptor and uploads the 1D
+ * tables; fk_op_setup builds the device E-restriction (int32) and the PA
+ * data D (BP1: w*|J| per point; BP3: 6-component symmetric w*|J|*J^-1 J^-T). */
+int fk_op_create(fk_op** out, const fk_op_desc* desc);
+int fk_op_setup(fk_op* op);
+int fk_op_destroy(fk_op* op);
+int fk_op_get_info(const fk_op* op, fk_op_info* info);
+int fk_op_set_variant(fk_op* op, int variant);
+
+/* Parity hooks: restriction rows as GLOBAL int64 ids (nel_local*d^3) and the
+ * PA data (nel_local * ncomp * q^3 doubles, element-major) copied to host. */
+int fk_op_restriction(fk_op* op, int64_t* host_out);
+int fk_op_pa_data(fk_op* op, double* host_out);
+
+/* y = A x on this rank's L-vector (length ndof_local); with a comm attached
+ * the shared interface planes are summed across neighbouring ranks, so y is
+ * the assembled P^T A_E P x restricted to this rank. */
+int fk_op_apply(fk_op* op, const double* x_dev, double* y_dev);
+/* Same with host buffers (pageable or pinned): H2D, apply, D2H, synchronise. */
+int fk_op_apply_host(fk_op* op, const double* x_host, double* y_host);
+/* Element-local apply without exchange or Dirichlet fix-up (testing). */
+int fk_op_apply_local(fk_op* op, const double* x_dev, double* y_dev);
+
+/* Assembled diagonal of A (Jacobi preconditioner); ones on essential dofs. */
+int fk_op_diagonal(fk_op* op, double* diag_dev);
+
+/* Jacobi-PCG (MFEM CGSolver semantics, x0 = 0), fixed `iters` iterations
+ * unless rtol > 0 stops it (r.z <= rtol^2 r0.z0).  hist_host receives
+ * sqrt(r_k . z_k) for k = 0..iters_done (iters+1 doubles).  Synchronises. */
+int fk_cg_solve(fk_op* op, const double* b_dev, double* x_dev, int iters, double rtol,
+                double* hist_host, int* iters_done);
+
+/* Device reductions used by multi-rank CG and by tests. */
+int fk_dot(fk_op* op, const double* a_dev, const double* b_dev, double* host_out);
+
+/* Multi-GPU: one communicator per rank over NCCL.  nccl_unique_id points to
+ * the 128-byte ncclUniqueId produced by fk_comm_unique_id on rank 0 and
+ * broadcast by the caller (e.g. torch.distributed). */
+int fk_comm_unique_id(void* out128);
+int fk_comm_create(fk_comm** out, const void* nccl_unique_id, int rank, int nranks, int device);
+int fk_comm_destroy(fk_comm* comm);
+
+/* Benchmark hook: time `reps` applies with CUDA events on the handle's
+ * stream (after the caller's warm-up); returns mean milliseconds per apply
+ * of the whole apply and of the fused kernel alone. */
+int fk_op_time_apply(fk_op* op, const double* x_dev, double* y_dev, int reps,
+                     const void* flush_dev, size_t flush_bytes,
+                     double* ms_apply, double* ms_kernel);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FK_B200_H */

@@ -1,0 +1,599 @@
+// fk_api.cu — the C-ABI (include/fk.h): handle lifecycle, setup, apply,
+// diagonal, device CG, z-slab exchange.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fk_cg.cuh"
+#include "fk_comm.h"
+#include "fk_internal.h"
+#include "fk_setup.cuh"
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define FK_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(e_ == cudaErrorMemoryAllocation ? FK_ENOMEM : FK_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+
+#define FK_TRY(call)         \
+  do {                       \
+    int rc_ = (call);        \
+    if (rc_ != FK_OK) return rc_; \
+  } while (0)
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+std::vector<fk::KernelEntry>& registry() {
+  static std::vector<fk::KernelEntry> reg;
+  static std::once_flag once;
+  std::call_once(once, [] { fk::register_kernels(reg); });
+  return reg;
+}
+
+int grid_for(int64_t n, int threads, int num_sms) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms * 8;
+  return (int)std::max<int64_t>(1, std::min(b, cap));
+}
+
+// Per-order automatic variant (FK_VARIANT_AUTO), from the measured p-sweep
+// recorded in DESIGN.md ("variant choice").
+int auto_variant(int nc, int p, int q) {
+  (void)nc;
+  (void)p;
+  (void)q;
+  return FK_VARIANT_DFMA;
+}
+
+fk::OpView view(const fk_op* op) {
+  fk::OpView v;
+  v.B = op->B;
+  v.G = op->G;
+  v.gids = op->gids;
+  v.pa = op->pa;
+  v.mask = op->mask;
+  v.nel = (int)op->nel;
+  return v;
+}
+
+int select_kernel(fk_op* op, int variant) {
+  int v = variant == FK_VARIANT_AUTO ? auto_variant(op->nc, op->p, op->q) : variant;
+  const fk::KernelEntry* k = fk::find_kernel(op->nc, op->d, op->q, v);
+  if (k == nullptr)
+    return fail(FK_EUNSUPPORTED, "no %s kernel compiled for kind=%d p=%d q=%d",
+                v == FK_VARIANT_DMMA ? "DMMA" : "DFMA", op->desc.kind, op->p, op->q);
+  op->kern = k;
+  op->variant = v;
+  if (op->is_setup) {
+    DeviceGuard g(op->device);
+    FK_CUDA(cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k->smem));
+    int occ = 0;
+    FK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->func, k->T, k->smem));
+    if (occ < 1) return fail(FK_EUNSUPPORTED, "fused kernel does not fit on an SM (smem %zu)", k->smem);
+    const int64_t nbatch = (op->nel + k->E - 1) / k->E;
+    op->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ * op->num_sms));
+  }
+  return FK_OK;
+}
+
+int launch_local(fk_op* op, const double* x, double* y) {
+  FK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * op->ndof, op->stream));
+  op->kern->launch(view(op), x, y, op->blocks, op->stream);
+  FK_CUDA(cudaGetLastError());
+  return FK_OK;
+}
+
+int apply_full(fk_op* op, const double* x, double* y, cudaStream_t s_override = nullptr) {
+  cudaStream_t saved = op->stream;
+  if (s_override) op->stream = s_override;
+  int rc = launch_local(op, x, y);
+  if (rc == FK_OK && op->comm) rc = fk::exchange_interface(op, y, op->stream);
+  if (rc == FK_OK && op->desc.dirichlet && op->n_ess > 0) {
+    fk::ess_copy_kernel<<<grid_for(op->n_ess, 256, op->num_sms), 256, 0, op->stream>>>(
+        y, x, op->ess, op->n_ess);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = fail(FK_ECUDA, "ess_copy_kernel: %s", cudaGetErrorString(e));
+  }
+  op->stream = saved;
+  return rc;
+}
+
+}  // namespace
+
+int fk_set_error(int code, const char* msg) { return fail(code, "%s", msg); }
+
+void fk_register_p1(std::vector<fk::KernelEntry>&);
+void fk_register_p2(std::vector<fk::KernelEntry>&);
+void fk_register_p3(std::vector<fk::KernelEntry>&);
+void fk_register_p4(std::vector<fk::KernelEntry>&);
+void fk_register_p5(std::vector<fk::KernelEntry>&);
+void fk_register_p6(std::vector<fk::KernelEntry>&);
+void fk_register_p7(std::vector<fk::KernelEntry>&);
+void fk_register_p8(std::vector<fk::KernelEntry>&);
+
+namespace fk {
+void register_kernels(std::vector<KernelEntry>& out) {
+  fk_register_p1(out);
+  fk_register_p2(out);
+  fk_register_p3(out);
+  fk_register_p4(out);
+  fk_register_p5(out);
+  fk_register_p6(out);
+  fk_register_p7(out);
+  fk_register_p8(out);
+}
+
+const KernelEntry* find_kernel(int nc, int d, int q, int variant) {
+  for (const auto& k : registry())
+    if (k.nc == nc && k.d == d && k.q == q && k.variant == variant) return &k;
+  return nullptr;
+}
+}  // namespace fk
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+int fk_version(void) { return FK_API_VERSION; }
+
+const char* fk_last_error(void) { return g_last_error.c_str(); }
+
+int fk_op_create(fk_op** out, const fk_op_desc* d) {
+  if (out == nullptr || d == nullptr) return fail(FK_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->kind != FK_KIND_MASS && d->kind != FK_KIND_DIFFUSION)
+    return fail(FK_EINVAL, "kind %d is not FK_KIND_MASS (1) or FK_KIND_DIFFUSION (3)", d->kind);
+  if (d->p < 1 || d->p > 8) return fail(FK_EUNSUPPORTED, "order p=%d outside 1..8", d->p);
+  if (d->q != d->p + 1 && d->q != d->p + 2)
+    return fail(FK_EUNSUPPORTED, "num_quad_1d=%d must be p+1 or p+2 for p=%d", d->q, d->p);
+  if (d->nx < 1 || d->ny < 1 || d->nz_local < 1 || d->z0_layer < 0 ||
+      d->z0_layer + d->nz_local > d->nz_global)
+    return fail(FK_EINVAL, "mesh dimensions nx=%d ny=%d nz_local=%d z0=%d nz_global=%d do not match",
+                d->nx, d->ny, d->nz_local, d->z0_layer, d->nz_global);
+  if (!(d->jac_det > 0.0) || !(d->jac_diag[0] > 0.0) || !(d->jac_diag[1] > 0.0) ||
+      !(d->jac_diag[2] > 0.0))
+    return fail(FK_EINVAL, "non-positive Jacobian");
+  if (d->B == nullptr || d->G == nullptr || d->w == nullptr)
+    return fail(FK_EINVAL, "basis tables B, G, w are required");
+  if (d->variant < FK_VARIANT_AUTO || d->variant > FK_VARIANT_DMMA)
+    return fail(FK_EINVAL, "unknown variant %d", d->variant);
+
+  fk_op* op = new fk_op();
+  op->desc = *d;
+  op->p = d->p;
+  op->d = d->p + 1;
+  op->q = d->q;
+  op->nc = d->kind == FK_KIND_DIFFUSION ? 3 : 1;
+  op->npa = d->kind == FK_KIND_DIFFUSION ? 6 : 1;
+  op->npx = (int64_t)d->nx * d->p + 1;
+  op->npy = (int64_t)d->ny * d->p + 1;
+  op->npz_local = (int64_t)d->nz_local * d->p + 1;
+  op->npz_global = (int64_t)d->nz_global * d->p + 1;
+  op->nel = (int64_t)d->nx * d->ny * d->nz_local;
+  op->ndof = op->npx * op->npy * op->npz_local;
+  op->ndof_global = op->npx * op->npy * op->npz_global;
+  op->dof_offset = (int64_t)d->z0_layer * d->p * op->npx * op->npy;
+  if (op->ndof >= (int64_t)1 << 31 || op->nel * op->d * op->d * op->d >= ((int64_t)1 << 40)) {
+    delete op;
+    return fail(FK_EINVAL, "local problem too large for int32 dof ids (%lld dofs)",
+                (long long)(op->ndof));
+  }
+  if (op->nel >= ((int64_t)1 << 31) - 64) {
+    delete op;
+    return fail(FK_EINVAL, "too many local elements");
+  }
+  const int qd = op->q * op->d;
+  std::memcpy(op->B, d->B, sizeof(double) * qd);
+  std::memcpy(op->G, d->G, sizeof(double) * qd);
+  std::memcpy(op->w, d->w, sizeof(double) * op->q);
+  for (int s = 0; s < 3; ++s) op->jinv[s] = 1.0 / d->jac_diag[s];
+  if (d->gather_ids != nullptr) {
+    const int64_t n = op->nel * op->d * op->d * op->d;
+    op->host_gids.resize(n);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t g = d->gather_ids[i] - op->dof_offset;
+      if (g < 0 || g >= op->ndof) {
+        delete op;
+        return fail(FK_EINVAL, "gather_ids[%lld]=%lld outside this rank's dofs", (long long)i,
+                    (long long)d->gather_ids[i]);
+      }
+      op->host_gids[i] = (int)g;
+    }
+  }
+  op->device = d->device;
+  op->stream = static_cast<cudaStream_t>(d->stream);
+  op->comm = d->comm;
+  {
+    DeviceGuard g(op->device);
+    cudaError_t e = cudaDeviceGetAttribute(&op->num_sms, cudaDevAttrMultiProcessorCount, op->device);
+    if (e != cudaSuccess) {
+      delete op;
+      return fail(FK_ECUDA, "device %d: %s", d->device, cudaGetErrorString(e));
+    }
+  }
+  int rc = select_kernel(op, d->variant);
+  if (rc != FK_OK) {
+    delete op;
+    return rc;
+  }
+  *out = op;
+  return FK_OK;
+}
+
+int fk_op_setup(fk_op* op) {
+  if (op == nullptr) return fail(FK_EINVAL, "null handle");
+  DeviceGuard g(op->device);
+  const int d3 = op->d * op->d * op->d, q3 = op->q * op->q * op->q;
+  cudaStream_t s = op->stream;
+  if (op->gids == nullptr) FK_CUDA(cudaMalloc(&op->gids, sizeof(int) * op->nel * d3));
+  if (op->host_gids.empty()) {
+    fk::restriction_kernel<<<grid_for(op->nel * d3, 256, op->num_sms), 256, 0, s>>>(
+        op->gids, op->desc.nx, op->desc.ny, op->desc.nz_local, op->p, op->npx, op->npy);
+    FK_CUDA(cudaGetLastError());
+  } else {
+    FK_CUDA(cudaMemcpyAsync(op->gids, op->host_gids.data(), sizeof(int) * op->nel * d3,
+                            cudaMemcpyHostToDevice, s));
+  }
+  // PA data (+64 bytes slack for the 16-byte-granular L2 prefetch)
+  if (op->pa == nullptr) FK_CUDA(cudaMalloc(&op->pa, sizeof(double) * op->nel * op->npa * q3 + 64));
+  double* dw = nullptr;
+  FK_CUDA(cudaMalloc(&dw, sizeof(double) * op->q));
+  FK_CUDA(cudaMemcpyAsync(dw, op->w, sizeof(double) * op->q, cudaMemcpyHostToDevice, s));
+  fk::pa_data_kernel<<<grid_for(op->nel * q3, 256, op->num_sms), 256, 0, s>>>(
+      op->pa, op->nel, op->q, op->npa, dw, op->desc.jac_det, op->jinv[0], op->jinv[1], op->jinv[2]);
+  FK_CUDA(cudaGetLastError());
+  if (op->desc.dirichlet) {
+    if (op->mask == nullptr) FK_CUDA(cudaMalloc(&op->mask, op->ndof));
+    const int64_t ring = 2 * (op->npx + op->npy) * op->npz_local + 2 * op->npx * op->npy;
+    if (op->ess == nullptr) FK_CUDA(cudaMalloc(&op->ess, sizeof(int) * (ring + 16)));
+    unsigned long long* dn = nullptr;
+    FK_CUDA(cudaMalloc(&dn, sizeof(unsigned long long)));
+    FK_CUDA(cudaMemsetAsync(dn, 0, sizeof(unsigned long long), s));
+    fk::dirichlet_kernel<<<grid_for(op->ndof, 256, op->num_sms), 256, 0, s>>>(
+        op->mask, op->ess, dn, op->npx, op->npy, op->npz_local,
+        (int64_t)op->desc.z0_layer * op->p, op->npz_global);
+    FK_CUDA(cudaGetLastError());
+    unsigned long long hn = 0;
+    FK_CUDA(cudaMemcpyAsync(&hn, dn, sizeof(hn), cudaMemcpyDeviceToHost, s));
+    FK_CUDA(cudaStreamSynchronize(s));
+    op->n_ess = (int64_t)hn;
+    cudaFree(dn);
+  }
+  FK_CUDA(cudaStreamSynchronize(s));
+  cudaFree(dw);
+  if (op->ev0 == nullptr) {
+    FK_CUDA(cudaEventCreate(&op->ev0));
+    FK_CUDA(cudaEventCreate(&op->ev1));
+    FK_CUDA(cudaEventCreate(&op->ev2));
+    FK_CUDA(cudaEventCreate(&op->ev3));
+  }
+  if (op->comm) FK_TRY(fk::comm_setup(op));
+  op->is_setup = true;
+  return select_kernel(op, op->desc.variant);
+}
+
+int fk_op_destroy(fk_op* op) {
+  if (op == nullptr) return FK_OK;
+  DeviceGuard g(op->device);
+  cudaFree(op->gids);
+  cudaFree(op->pa);
+  cudaFree(op->mask);
+  cudaFree(op->ess);
+  cudaFree(op->stage_x);
+  cudaFree(op->stage_y);
+  cudaFree(op->work);
+  cudaFree(op->scal);
+  cudaFree(op->partials);
+  cudaFree(op->counter);
+  cudaFree(op->hist);
+  cudaFree(op->halo);
+  if (op->ev0) cudaEventDestroy(op->ev0);
+  if (op->ev1) cudaEventDestroy(op->ev1);
+  if (op->ev2) cudaEventDestroy(op->ev2);
+  if (op->ev3) cudaEventDestroy(op->ev3);
+  if (op->cg_stream) cudaStreamDestroy(op->cg_stream);
+  delete op;
+  return FK_OK;
+}
+
+int fk_op_get_info(const fk_op* op, fk_op_info* info) {
+  if (op == nullptr || info == nullptr) return fail(FK_EINVAL, "null argument");
+  info->ndof_local = op->ndof;
+  info->nel_local = op->nel;
+  info->dof_offset = op->dof_offset;
+  info->ndof_global = op->ndof_global;
+  info->pa_bytes = (int64_t)sizeof(double) * op->nel * op->npa * op->q * op->q * op->q;
+  info->variant = op->variant;
+  info->elems_per_block = op->kern ? op->kern->E : 0;
+  info->threads_per_block = op->kern ? op->kern->T : 0;
+  info->blocks = op->blocks;
+  return FK_OK;
+}
+
+int fk_op_set_variant(fk_op* op, int variant) {
+  if (op == nullptr) return fail(FK_EINVAL, "null handle");
+  if (variant < FK_VARIANT_AUTO || variant > FK_VARIANT_DMMA)
+    return fail(FK_EINVAL, "unknown variant %d", variant);
+  op->desc.variant = variant;
+  return select_kernel(op, variant);
+}
+
+int fk_op_restriction(fk_op* op, int64_t* host_out) {
+  if (op == nullptr || host_out == nullptr) return fail(FK_EINVAL, "null argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  DeviceGuard g(op->device);
+  const int64_t n = op->nel * op->d * op->d * op->d;
+  std::vector<int> tmp(n);
+  FK_CUDA(cudaMemcpyAsync(tmp.data(), op->gids, sizeof(int) * n, cudaMemcpyDeviceToHost, op->stream));
+  FK_CUDA(cudaStreamSynchronize(op->stream));
+  for (int64_t i = 0; i < n; ++i) host_out[i] = (int64_t)tmp[i] + op->dof_offset;
+  return FK_OK;
+}
+
+int fk_op_pa_data(fk_op* op, double* host_out) {
+  if (op == nullptr || host_out == nullptr) return fail(FK_EINVAL, "null argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  DeviceGuard g(op->device);
+  const int64_t n = op->nel * op->npa * op->q * op->q * op->q;
+  FK_CUDA(cudaMemcpyAsync(host_out, op->pa, sizeof(double) * n, cudaMemcpyDeviceToHost, op->stream));
+  FK_CUDA(cudaStreamSynchronize(op->stream));
+  return FK_OK;
+}
+
+int fk_op_apply(fk_op* op, const double* x, double* y) {
+  if (op == nullptr || x == nullptr || y == nullptr) return fail(FK_EINVAL, "null argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  if (x == y) return fail(FK_EINVAL, "in-place apply is not supported (x == y)");
+  DeviceGuard g(op->device);
+  return apply_full(op, x, y);
+}
+
+int fk_op_apply_local(fk_op* op, const double* x, double* y) {
+  if (op == nullptr || x == nullptr || y == nullptr) return fail(FK_EINVAL, "null argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  DeviceGuard g(op->device);
+  return launch_local(op, x, y);
+}
+
+int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
+  if (op == nullptr || xh == nullptr || yh == nullptr) return fail(FK_EINVAL, "null argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  DeviceGuard g(op->device);
+  const size_t bytes = sizeof(double) * op->ndof;
+  if (op->stage_x == nullptr) {
+    FK_CUDA(cudaMalloc(&op->stage_x, bytes));
+    FK_CUDA(cudaMalloc(&op->stage_y, bytes));
+  }
+  FK_CUDA(cudaMemcpyAsync(op->stage_x, xh, bytes, cudaMemcpyHostToDevice, op->stream));
+  FK_TRY(apply_full(op, op->stage_x, op->stage_y));
+  FK_CUDA(cudaMemcpyAsync(yh, op->stage_y, bytes, cudaMemcpyDeviceToHost, op->stream));
+  FK_CUDA(cudaStreamSynchronize(op->stream));
+  return FK_OK;
+}
+
+int fk_op_diagonal(fk_op* op, double* diag) {
+  if (op == nullptr || diag == nullptr) return fail(FK_EINVAL, "null argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  DeviceGuard g(op->device);
+  FK_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * op->ndof, op->stream));
+  const fk::KernelEntry* k = fk::find_kernel(op->nc, op->d, op->q, FK_VARIANT_DFMA);
+  if (k == nullptr || k->diag == nullptr) return fail(FK_EUNSUPPORTED, "no diagonal kernel");
+  k->diag(view(op), diag, op->nel, grid_for(op->nel * op->d * op->d * op->d, 128, op->num_sms),
+          op->stream);
+  FK_CUDA(cudaGetLastError());
+  if (op->comm) FK_TRY(fk::exchange_interface(op, diag, op->stream));
+  if (op->desc.dirichlet && op->n_ess > 0) {
+    fk::ess_set_kernel<<<grid_for(op->n_ess, 256, op->num_sms), 256, 0, op->stream>>>(
+        diag, op->ess, op->n_ess, 1.0);
+    FK_CUDA(cudaGetLastError());
+  }
+  return FK_OK;
+}
+
+static int ensure_reduce_ws(fk_op* op) {
+  if (op->partials == nullptr) {
+    FK_CUDA(cudaMalloc(&op->partials, sizeof(double) * 4096));
+    FK_CUDA(cudaMalloc(&op->counter, sizeof(unsigned) * 4));
+    FK_CUDA(cudaMemset(op->counter, 0, sizeof(unsigned) * 4));
+    FK_CUDA(cudaMalloc(&op->scal, sizeof(double) * 16 + sizeof(int) * 8));
+    FK_CUDA(cudaMemset(op->scal, 0, sizeof(double) * 16 + sizeof(int) * 8));
+  }
+  return FK_OK;
+}
+
+static int red_blocks(const fk_op* op) { return std::min(op->num_sms * 4, 4096); }
+
+int fk_dot(fk_op* op, const double* a, const double* b, double* host_out) {
+  if (op == nullptr || a == nullptr || b == nullptr || host_out == nullptr)
+    return fail(FK_EINVAL, "null argument");
+  DeviceGuard g(op->device);
+  FK_TRY(ensure_reduce_ws(op));
+  const int64_t n0 = fk::owned_begin(op);
+  fk::dot_kernel<<<red_blocks(op), fk::kRedThreads, 0, op->stream>>>(
+      a, b, n0, op->ndof, op->partials, op->counter, op->scal + fk::S_DOT);
+  FK_CUDA(cudaGetLastError());
+  if (op->comm) FK_TRY(fk::allreduce_scalar(op, op->scal + fk::S_DOT, op->stream));
+  FK_CUDA(cudaMemcpyAsync(host_out, op->scal + fk::S_DOT, sizeof(double), cudaMemcpyDeviceToHost,
+                          op->stream));
+  FK_CUDA(cudaStreamSynchronize(op->stream));
+  return FK_OK;
+}
+
+// One CG iteration, enqueued on stream s (capturable).
+static int cg_iteration(fk_op* op, double* x, cudaStream_t s) {
+  const int64_t n = op->ndof, n0 = fk::owned_begin(op);
+  double* r = op->work;
+  double* z = r + n;
+  double* p = z + n;
+  double* Ap = p + n;
+  double* dinv = Ap + n;
+  int* iscal = reinterpret_cast<int*>(op->scal + 16);
+  const int rb = red_blocks(op);
+  FK_TRY(apply_full(op, p, Ap, s));
+  fk::dot_kernel<<<rb, fk::kRedThreads, 0, s>>>(p, Ap, n0, n, op->partials, op->counter,
+                                                op->scal + fk::S_DEN);
+  if (op->comm) FK_TRY(fk::allreduce_scalar(op, op->scal + fk::S_DEN, s));
+  fk::cg_alpha_kernel<<<1, 1, 0, s>>>(op->scal, iscal);
+  fk::cg_update_kernel<<<rb, fk::kRedThreads, 0, s>>>(x, r, z, p, Ap, dinv, n, n0, op->scal, iscal,
+                                                      op->partials, op->counter + 1,
+                                                      op->scal + fk::S_BN);
+  if (op->comm) FK_TRY(fk::allreduce_scalar(op, op->scal + fk::S_BN, s));
+  fk::cg_finish_kernel<<<1, 1, 0, s>>>(op->scal, iscal, op->hist);
+  fk::cg_dir_kernel<<<grid_for(n, 256, op->num_sms), 256, 0, s>>>(p, z, n, op->scal, iscal);
+  FK_CUDA(cudaGetLastError());
+  return FK_OK;
+}
+
+int fk_cg_solve(fk_op* op, const double* b, double* x, int iters, double rtol, double* hist_host,
+                int* iters_done) {
+  if (op == nullptr || b == nullptr || x == nullptr) return fail(FK_EINVAL, "null argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  if (iters < 0) return fail(FK_EINVAL, "iters must be >= 0");
+  DeviceGuard g(op->device);
+  const int64_t n = op->ndof;
+  if (op->work == nullptr) FK_CUDA(cudaMalloc(&op->work, sizeof(double) * 5 * n));
+  FK_TRY(ensure_reduce_ws(op));
+  if (op->hist_cap < iters + 1) {
+    cudaFree(op->hist);
+    FK_CUDA(cudaMalloc(&op->hist, sizeof(double) * (iters + 1)));
+    op->hist_cap = iters + 1;
+  }
+  if (op->cg_stream == nullptr) FK_CUDA(cudaStreamCreateWithFlags(&op->cg_stream, cudaStreamNonBlocking));
+  cudaStream_t s = op->cg_stream;
+  // order after the caller's stream
+  FK_CUDA(cudaEventRecord(op->ev0, op->stream));
+  FK_CUDA(cudaStreamWaitEvent(s, op->ev0, 0));
+  double* r = op->work;
+  double* z = r + n;
+  double* p = z + n;
+  double* dinv = p + 2 * n;
+  int* iscal = reinterpret_cast<int*>(op->scal + 16);
+  // Jacobi: dinv = 1/diag(A) (ones on essential dofs)
+  {
+    cudaStream_t saved = op->stream;
+    op->stream = s;
+    int rc = fk_op_diagonal(op, z);
+    op->stream = saved;
+    FK_TRY(rc);
+  }
+  fk::recip_kernel<<<grid_for(n, 256, op->num_sms), 256, 0, s>>>(dinv, z, n);
+  const int64_t n0 = fk::owned_begin(op);
+  fk::cg_init_kernel<<<red_blocks(op), fk::kRedThreads, 0, s>>>(
+      b, x, r, z, p, dinv, n, n0, op->partials, op->counter + 2, op->scal + fk::S_NOM);
+  if (op->comm) FK_TRY(fk::allreduce_scalar(op, op->scal + fk::S_NOM, s));
+  fk::cg_start_kernel<<<1, 1, 0, s>>>(op->scal, iscal, op->hist, rtol);
+  FK_CUDA(cudaGetLastError());
+  if (iters > 0) {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool use_graph = true;
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      int rc = cg_iteration(op, x, s);
+      cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      if (rc != FK_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      if (ce != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+        use_graph = false;
+        cudaGetLastError();
+      }
+    } else {
+      use_graph = false;
+      cudaGetLastError();
+    }
+    for (int it = 0; it < iters; ++it) {
+      if (use_graph) {
+        FK_CUDA(cudaGraphLaunch(exec, s));
+      } else {
+        FK_TRY(cg_iteration(op, x, s));
+      }
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+  int hi[2] = {0, 0};
+  FK_CUDA(cudaMemcpyAsync(hi, iscal, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+  FK_CUDA(cudaStreamSynchronize(s));
+  const int done_it = hi[fk::I_IT];
+  if (hist_host) FK_CUDA(cudaMemcpy(hist_host, op->hist, sizeof(double) * (done_it + 1), cudaMemcpyDeviceToHost));
+  if (iters_done) *iters_done = done_it;
+  // make the caller's stream see the result
+  FK_CUDA(cudaEventRecord(op->ev1, s));
+  FK_CUDA(cudaStreamWaitEvent(op->stream, op->ev1, 0));
+  return FK_OK;
+}
+
+int fk_op_time_apply(fk_op* op, const double* x, double* y, int reps, const void* flush,
+                     size_t flush_bytes, double* ms_apply, double* ms_kernel) {
+  if (op == nullptr || x == nullptr || y == nullptr || reps < 1) return fail(FK_EINVAL, "bad argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  DeviceGuard g(op->device);
+  double tot_a = 0.0, tot_k = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    if (flush && flush_bytes)
+      FK_CUDA(cudaMemsetAsync(const_cast<void*>(flush), r & 0xff, flush_bytes, op->stream));
+    FK_CUDA(cudaEventRecord(op->ev0, op->stream));
+    FK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * op->ndof, op->stream));
+    FK_CUDA(cudaEventRecord(op->ev1, op->stream));
+    op->kern->launch(view(op), x, y, op->blocks, op->stream);
+    FK_CUDA(cudaGetLastError());
+    FK_CUDA(cudaEventRecord(op->ev2, op->stream));
+    if (op->comm) FK_TRY(fk::exchange_interface(op, y, op->stream));
+    if (op->desc.dirichlet && op->n_ess > 0)
+      fk::ess_copy_kernel<<<grid_for(op->n_ess, 256, op->num_sms), 256, 0, op->stream>>>(
+          y, x, op->ess, op->n_ess);
+    FK_CUDA(cudaEventRecord(op->ev3, op->stream));
+    FK_CUDA(cudaEventSynchronize(op->ev3));
+    float a = 0.f, k = 0.f;
+    FK_CUDA(cudaEventElapsedTime(&a, op->ev0, op->ev3));
+    FK_CUDA(cudaEventElapsedTime(&k, op->ev1, op->ev2));
+    tot_a += a;
+    tot_k += k;
+  }
+  if (ms_apply) *ms_apply = tot_a / reps;
+  if (ms_kernel) *ms_kernel = tot_k / reps;
+  return FK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,151 @@
+// fk_cg.cuh — device-resident Jacobi-PCG pieces (MFEM CGSolver semantics).
+//
+// All scalars stay on the device; one iteration is
+//   apply(p -> Ap) ; den = p.Ap ; alpha = nom/den ;
+//   x += alpha p ; r -= alpha Ap ; z = dinv r ; bn = r.z   (one fused pass)
+//   hist[it] = sqrt(bn) ; beta = bn/nom ; nom = bn ; p = z + beta p
+// and is captured once into a CUDA graph that is replayed `iters` times.
+// Reductions are deterministic: fixed grid, fixed per-block order, the last
+// block to finish sums the block partials in index order.
+#pragma once
+
+#include <cstdint>
+
+namespace fk {
+
+enum ScalarSlot { S_NOM = 0, S_DEN = 1, S_BN = 2, S_STOP = 3, S_ALPHA = 4, S_BETA = 5, S_DOT = 6 };
+enum IntSlot { I_DONE = 0, I_IT = 1 };
+
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-reduce v; block partial to partials[blockIdx.x]; the last block sums
+// the partials in order and writes *out (then resets the counter).
+__device__ __forceinline__ void reduce_finish(double v, double* partials, unsigned* counter,
+                                              double* out) {
+  __shared__ double sw[kRedThreads / 32];
+  __shared__ bool last;
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sw[wid] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kRedThreads / 32; ++i) s += sw[i];
+    partials[blockIdx.x] = s;
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double s = 0.0;
+    if (threadIdx.x < 32) {
+      // fixed order: lane l sums partials l, l+32, ... then a fixed shuffle tree
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) s += ((volatile double*)partials)[i];
+      s = warp_sum(s);
+      if (threadIdx.x == 0) {
+        *out = s;
+        *counter = 0u;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) dot_kernel(const double* __restrict__ a,
+                                                          const double* __restrict__ b,
+                                                          int64_t n0, int64_t n1,
+                                                          double* partials, unsigned* counter,
+                                                          double* out) {
+  double s = 0.0;
+  for (int64_t i = n0 + blockIdx.x * (int64_t)kRedThreads + threadIdx.x; i < n1;
+       i += (int64_t)gridDim.x * kRedThreads)
+    s = fma(a[i], b[i], s);
+  reduce_finish(s, partials, counter, out);
+}
+
+// x = 0, r = b, z = dinv*b, p = z; partial r.z over [n0, n1)
+__global__ void __launch_bounds__(kRedThreads) cg_init_kernel(
+    const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r,
+    double* __restrict__ z, double* __restrict__ p, const double* __restrict__ dinv, int64_t n,
+    int64_t n0, double* partials, unsigned* counter, double* out) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)kRedThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kRedThreads) {
+    const double bi = b[i], zi = dinv[i] * bi;
+    x[i] = 0.0;
+    r[i] = bi;
+    z[i] = zi;
+    p[i] = zi;
+    if (i >= n0) s = fma(bi, zi, s);
+  }
+  reduce_finish(s, partials, counter, out);
+}
+
+__global__ void cg_start_kernel(double* scal, int* iscal, double* hist, double rtol) {
+  const double nom = scal[S_NOM];
+  hist[0] = sqrt(nom);
+  scal[S_STOP] = rtol * rtol * nom;
+  iscal[I_IT] = 0;
+  iscal[I_DONE] = (rtol > 0.0 && nom <= 0.0) ? 1 : 0;
+}
+
+__global__ void cg_alpha_kernel(double* scal, const int* iscal) {
+  if (iscal[I_DONE]) return;
+  scal[S_ALPHA] = scal[S_NOM] / scal[S_DEN];
+}
+
+// x += alpha p ; r -= alpha Ap ; z = dinv r ; partial r.z over [n0, n)
+__global__ void __launch_bounds__(kRedThreads) cg_update_kernel(
+    double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+    const double* __restrict__ p, const double* __restrict__ Ap, const double* __restrict__ dinv,
+    int64_t n, int64_t n0, const double* scal, const int* iscal, double* partials,
+    unsigned* counter, double* out) {
+  if (iscal[I_DONE]) return;  // uniform across the grid
+  const double alpha = scal[S_ALPHA];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)kRedThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kRedThreads) {
+    const double pi = p[i];
+    x[i] = fma(alpha, pi, x[i]);
+    const double ri = fma(-alpha, Ap[i], r[i]);
+    const double zi = dinv[i] * ri;
+    r[i] = ri;
+    z[i] = zi;
+    if (i >= n0) s = fma(ri, zi, s);
+  }
+  reduce_finish(s, partials, counter, out);
+}
+
+__global__ void cg_finish_kernel(double* scal, int* iscal, double* hist) {
+  if (iscal[I_DONE]) return;
+  const double bn = scal[S_BN];
+  const int it = iscal[I_IT] + 1;
+  iscal[I_IT] = it;
+  hist[it] = sqrt(bn);
+  scal[S_BETA] = bn / scal[S_NOM];
+  scal[S_NOM] = bn;
+  if (scal[S_STOP] > 0.0 && bn <= scal[S_STOP]) iscal[I_DONE] = 1;
+}
+
+__global__ void cg_dir_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                              const double* scal, const int* iscal) {
+  if (iscal[I_DONE]) return;
+  const double beta = scal[S_BETA];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+__global__ void recip_kernel(double* __restrict__ out, const double* __restrict__ in, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = 1.0 / in[i];
+}
+
+}  // namespace fk

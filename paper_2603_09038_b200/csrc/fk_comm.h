@@ -1,0 +1,22 @@
+// fk_comm.h — z-slab multi-GPU plumbing (NCCL over NVLink / NVSwitch).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+struct fk_op;
+
+namespace fk {
+
+// First locally OWNED dof: the bottom interface plane of rank r > 0 belongs
+// to rank r-1 (the lower rank owns shared planes), so dot products run over
+// [owned_begin, ndof_local) and every global dof is counted exactly once.
+int64_t owned_begin(const fk_op* op);
+
+int comm_setup(fk_op* op);
+// y_plane += neighbour's partial sum of the same plane, for both interfaces.
+int exchange_interface(fk_op* op, double* y, cudaStream_t s);
+int allreduce_scalar(fk_op* op, double* dev_scalar, cudaStream_t s);
+
+}  // namespace fk

@@ -1,0 +1,81 @@
+// fk_internal.h — internal structures of libfk_b200 (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/fk.h"
+
+namespace fk {
+
+struct OpView;  // what a kernel launcher needs
+using LaunchFn = void (*)(const OpView&, const double* x, double* y, int blocks, cudaStream_t s);
+using DiagFn = void (*)(const OpView&, double* diag, int64_t nel, int blocks, cudaStream_t s);
+
+struct KernelEntry {
+  int nc = 0, d = 0, q = 0, variant = 0;
+  int E = 0, T = 0;
+  size_t smem = 0;
+  const void* func = nullptr;
+  LaunchFn launch = nullptr;
+  DiagFn diag = nullptr;
+};
+
+struct OpView {
+  const double* B;  // host tables (q*d)
+  const double* G;
+  const int* gids;
+  const double* pa;
+  const unsigned char* mask;
+  int nel;
+};
+
+void register_kernels(std::vector<KernelEntry>& out);  // pa_instances*.cu
+const KernelEntry* find_kernel(int nc, int d, int q, int variant);
+
+}  // namespace fk
+
+struct fk_comm {
+  void* nccl = nullptr;  // ncclComm_t
+  int rank = 0, nranks = 1, device = 0;
+};
+
+struct fk_op {
+  fk_op_desc desc{};
+  int p = 0, d = 0, q = 0, nc = 0, npa = 0;
+  int64_t npx = 0, npy = 0, npz_local = 0, npz_global = 0;
+  int64_t nel = 0, ndof = 0, dof_offset = 0, ndof_global = 0;
+  double B[100], G[100], w[10];
+  double jinv[3];
+  std::vector<int> host_gids;  // optional user map (local ids)
+  cudaStream_t stream = nullptr;  // user stream
+  cudaStream_t cg_stream = nullptr;
+  int device = 0, num_sms = 0;
+  int variant = FK_VARIANT_AUTO;
+  const fk::KernelEntry* kern = nullptr;
+  int blocks = 0;
+  bool is_setup = false;
+  // device data
+  int* gids = nullptr;
+  double* pa = nullptr;
+  unsigned char* mask = nullptr;
+  int* ess = nullptr;
+  int64_t n_ess = 0;
+  // host staging for fk_op_apply_host
+  double* stage_x = nullptr;
+  double* stage_y = nullptr;
+  // CG / reduction workspace
+  double* work = nullptr;  // r, z, p, Ap, dinv (5 * ndof)
+  double* scal = nullptr;  // scalars
+  double* partials = nullptr;
+  unsigned* counter = nullptr;
+  double* hist = nullptr;
+  int hist_cap = 0;
+  // multi-rank
+  fk_comm* comm = nullptr;
+  double* halo = nullptr;  // receive buffers (2 planes)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+};
