@@ -377,14 +377,14 @@ def run_sweep(a, peak):
             op = PAOperator(build_mesh(n, n, n), p, kind=kind)
             x = torch.randn(op.num_dofs, dtype=torch.float64, device="cuda")
             y = torch.empty_like(x)
-            for variant in ("dfma", "dmma"):
+            for variant, cfg in (("dfma", 0), ("dfma", 1), ("dfma", 2), ("dmma", 0), ("dmma", 1)):
                 try:
-                    op.set_variant(variant)
+                    op.set_config(variant, cfg)
                 except NotImplementedError:
                     continue
                 op.time_apply(x, y, 5)
                 ms_a, ms_k = op.time_apply(x, y, 30)
-                rec = {"kind": kind, "p": p, "n": n, "variant": variant, "ndof": op.num_dofs,
+                rec = {"kind": kind, "p": p, "n": n, "variant": variant, "cfg": cfg, "ndof": op.num_dofs,
                        "ms_apply": ms_a, "ms_kernel": ms_k,
                        "gdofs": op.num_dofs / (ms_a * 1e-3) / 1e9,
                        "hbm_frac": op.bytes_per_apply / (ms_k * 1e-3) / 1e9 / peak,

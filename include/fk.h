@@ -97,6 +97,9 @@ int fk_op_setup(fk_op* op);
 int fk_op_destroy(fk_op* op);
 int fk_op_get_info(const fk_op* op, fk_op_info* info);
 int fk_op_set_variant(fk_op* op, int variant);
+/* Select one of the compiled launch geometries of a variant (cfg = 0 is the
+ * default; FK_EUNSUPPORTED when that cfg does not exist).  Tuning/testing. */
+int fk_op_set_config(fk_op* op, int variant, int cfg);
 
 /* Parity hooks: restriction rows as GLOBAL int64 ids (nel_local*d^3) and the
  * PA data (nel_local * ncomp * q^3 doubles, element-major) copied to host. */

@@ -33,7 +33,8 @@ VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 #: every symbol include/fk.h declares (checked by tests/test_cabi.py)
 EXPORTS = (
     "fk_version", "fk_last_error", "fk_op_create", "fk_op_setup", "fk_op_destroy",
-    "fk_op_get_info", "fk_op_set_variant", "fk_op_restriction", "fk_op_pa_data",
+    "fk_op_get_info", "fk_op_set_variant", "fk_op_set_config", "fk_op_restriction",
+    "fk_op_pa_data",
     "fk_op_apply", "fk_op_apply_host", "fk_op_apply_local", "fk_op_diagonal",
     "fk_cg_solve", "fk_dot", "fk_comm_unique_id", "fk_comm_create", "fk_comm_destroy",
     "fk_op_time_apply",
@@ -113,6 +114,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "fk_op_destroy": (i, [vp]),
         "fk_op_get_info": (i, [vp, ctypes.POINTER(FkOpInfo)]),
         "fk_op_set_variant": (i, [vp, i]),
+        "fk_op_set_config": (i, [vp, i, i]),
         "fk_op_restriction": (i, [vp, ctypes.POINTER(i64)]),
         "fk_op_pa_data": (i, [vp, pd]),
         "fk_op_apply": (i, [vp, vp, vp]),

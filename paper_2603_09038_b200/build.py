@@ -49,7 +49,7 @@ def nccl_include() -> list[str]:
 
 def flags() -> list[str]:
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-                   "-Xptxas", "-warn-spills", "-DFK_HAVE_DMMA=" + os.environ.get("FK_HAVE_DMMA", "0")] + nccl_include()
+                   "-Xptxas", "-warn-spills", ] + nccl_include()
 
 
 def sources():

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -88,17 +89,37 @@ fk::OpView view(const fk_op* op) {
   v.G = op->G;
   v.gids = op->gids;
   v.pa = op->pa;
-  v.mask = op->mask;
+  v.ebits = op->ebits;
   v.nel = (int)op->nel;
   return v;
 }
 
 int select_kernel(fk_op* op, int variant) {
   int v = variant == FK_VARIANT_AUTO ? auto_variant(op->nc, op->p, op->q) : variant;
-  const fk::KernelEntry* k = fk::find_kernel(op->nc, op->d, op->q, v);
+  const fk::KernelEntry* k = nullptr;
+  if (op->cfg >= 0) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, op->cfg);
+  if (k == nullptr) k = fk::find_kernel(op->nc, op->d, op->q, v);
   if (k == nullptr)
     return fail(FK_EUNSUPPORTED, "no %s kernel compiled for kind=%d p=%d q=%d",
                 v == FK_VARIANT_DMMA ? "DMMA" : "DFMA", op->desc.kind, op->p, op->q);
+  {
+    int max_smem = 0;
+    DeviceGuard g(op->device);
+    FK_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->device));
+    if (k->smem > (size_t)max_smem) {
+      if (op->cfg >= 0)
+        return fail(FK_EUNSUPPORTED, "launch config %d needs %zu B shared memory (> %d)", op->cfg,
+                    k->smem, max_smem);
+      // default geometry too large: first compiled geometry that fits
+      const fk::KernelEntry* alt = nullptr;
+      for (int c = 0; c < 8 && alt == nullptr; ++c) {
+        const fk::KernelEntry* t = fk::find_kernel_cfg(op->nc, op->d, op->q, v, c);
+        if (t && t->smem <= (size_t)max_smem) alt = t;
+      }
+      if (alt == nullptr) return fail(FK_EUNSUPPORTED, "no launch config fits in shared memory");
+      k = alt;
+    }
+  }
   op->kern = k;
   op->variant = v;
   if (op->is_setup) {
@@ -164,6 +185,12 @@ void register_kernels(std::vector<KernelEntry>& out) {
 const KernelEntry* find_kernel(int nc, int d, int q, int variant) {
   for (const auto& k : registry())
     if (k.nc == nc && k.d == d && k.q == q && k.variant == variant) return &k;
+  return nullptr;
+}
+
+const KernelEntry* find_kernel_cfg(int nc, int d, int q, int variant, int cfg) {
+  for (const auto& k : registry())
+    if (k.nc == nc && k.d == d && k.q == q && k.variant == variant && k.cfg == cfg) return &k;
   return nullptr;
 }
 }  // namespace fk
@@ -265,22 +292,31 @@ int fk_op_setup(fk_op* op) {
   DeviceGuard g(op->device);
   const int d3 = op->d * op->d * op->d, q3 = op->q * op->q * op->q;
   cudaStream_t s = op->stream;
-  if (op->gids == nullptr) FK_CUDA(cudaMalloc(&op->gids, sizeof(int) * op->nel * d3));
+  op->ps = fk::pa_stride(op->npa, op->q);
+  op->gs = fk::gid_stride(op->d);
+  op->ms = fk::bits_stride(op->d);
+  if (const char* c = std::getenv("FK_CFG")) op->cfg = std::atoi(c);
+  if (op->gids == nullptr) FK_CUDA(cudaMalloc(&op->gids, sizeof(int) * (op->nel * op->gs + 16)));
   if (op->host_gids.empty()) {
-    fk::restriction_kernel<<<grid_for(op->nel * d3, 256, op->num_sms), 256, 0, s>>>(
-        op->gids, op->desc.nx, op->desc.ny, op->desc.nz_local, op->p, op->npx, op->npy);
+    fk::restriction_kernel<<<grid_for(op->nel * op->gs, 256, op->num_sms), 256, 0, s>>>(
+        op->gids, op->desc.nx, op->desc.ny, op->desc.nz_local, op->p, op->npx, op->npy, op->gs);
     FK_CUDA(cudaGetLastError());
   } else {
-    FK_CUDA(cudaMemcpyAsync(op->gids, op->host_gids.data(), sizeof(int) * op->nel * d3,
+    std::vector<int> padded(op->nel * op->gs, 0);
+    for (int64_t e = 0; e < op->nel; ++e)
+      std::memcpy(&padded[e * op->gs], &op->host_gids[e * d3], sizeof(int) * d3);
+    FK_CUDA(cudaMemcpyAsync(op->gids, padded.data(), sizeof(int) * padded.size(),
                             cudaMemcpyHostToDevice, s));
+    FK_CUDA(cudaStreamSynchronize(s));
   }
-  // PA data (+64 bytes slack for the 16-byte-granular L2 prefetch)
-  if (op->pa == nullptr) FK_CUDA(cudaMalloc(&op->pa, sizeof(double) * op->nel * op->npa * q3 + 64));
+  // PA data, padded element stride (+64 bytes slack for 16-byte-granular copies)
+  if (op->pa == nullptr) FK_CUDA(cudaMalloc(&op->pa, sizeof(double) * op->nel * op->ps + 64));
   double* dw = nullptr;
   FK_CUDA(cudaMalloc(&dw, sizeof(double) * op->q));
   FK_CUDA(cudaMemcpyAsync(dw, op->w, sizeof(double) * op->q, cudaMemcpyHostToDevice, s));
   fk::pa_data_kernel<<<grid_for(op->nel * q3, 256, op->num_sms), 256, 0, s>>>(
-      op->pa, op->nel, op->q, op->npa, dw, op->desc.jac_det, op->jinv[0], op->jinv[1], op->jinv[2]);
+      op->pa, op->nel, op->q, op->npa, op->ps, dw, op->desc.jac_det, op->jinv[0], op->jinv[1],
+      op->jinv[2]);
   FK_CUDA(cudaGetLastError());
   if (op->desc.dirichlet) {
     if (op->mask == nullptr) FK_CUDA(cudaMalloc(&op->mask, op->ndof));
@@ -298,6 +334,10 @@ int fk_op_setup(fk_op* op) {
     FK_CUDA(cudaStreamSynchronize(s));
     op->n_ess = (int64_t)hn;
     cudaFree(dn);
+    if (op->ebits == nullptr) FK_CUDA(cudaMalloc(&op->ebits, sizeof(uint32_t) * (op->nel * op->ms + 16)));
+    fk::ebits_kernel<<<grid_for(op->nel * op->ms, 256, op->num_sms), 256, 0, s>>>(
+        op->ebits, op->gids, op->mask, op->nel, d3, op->gs, op->ms);
+    FK_CUDA(cudaGetLastError());
   }
   FK_CUDA(cudaStreamSynchronize(s));
   cudaFree(dw);
@@ -318,6 +358,7 @@ int fk_op_destroy(fk_op* op) {
   cudaFree(op->gids);
   cudaFree(op->pa);
   cudaFree(op->mask);
+  cudaFree(op->ebits);
   cudaFree(op->ess);
   cudaFree(op->stage_x);
   cudaFree(op->stage_y);
@@ -358,15 +399,28 @@ int fk_op_set_variant(fk_op* op, int variant) {
   return select_kernel(op, variant);
 }
 
+int fk_op_set_config(fk_op* op, int variant, int cfg) {
+  if (op == nullptr) return fail(FK_EINVAL, "null handle");
+  if (variant < FK_VARIANT_DFMA || variant > FK_VARIANT_DMMA || cfg < 0)
+    return fail(FK_EINVAL, "bad variant %d / cfg %d", variant, cfg);
+  if (fk::find_kernel_cfg(op->nc, op->d, op->q, variant, cfg) == nullptr)
+    return fail(FK_EUNSUPPORTED, "no launch config %d for variant %d", cfg, variant);
+  op->cfg = cfg;
+  op->desc.variant = variant;
+  return select_kernel(op, variant);
+}
+
 int fk_op_restriction(fk_op* op, int64_t* host_out) {
   if (op == nullptr || host_out == nullptr) return fail(FK_EINVAL, "null argument");
   if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
   DeviceGuard g(op->device);
-  const int64_t n = op->nel * op->d * op->d * op->d;
-  std::vector<int> tmp(n);
-  FK_CUDA(cudaMemcpyAsync(tmp.data(), op->gids, sizeof(int) * n, cudaMemcpyDeviceToHost, op->stream));
+  const int d3 = op->d * op->d * op->d;
+  std::vector<int> tmp(op->nel * op->gs);
+  FK_CUDA(cudaMemcpyAsync(tmp.data(), op->gids, sizeof(int) * tmp.size(), cudaMemcpyDeviceToHost,
+                          op->stream));
   FK_CUDA(cudaStreamSynchronize(op->stream));
-  for (int64_t i = 0; i < n; ++i) host_out[i] = (int64_t)tmp[i] + op->dof_offset;
+  for (int64_t e = 0; e < op->nel; ++e)
+    for (int l = 0; l < d3; ++l) host_out[e * d3 + l] = (int64_t)tmp[e * op->gs + l] + op->dof_offset;
   return FK_OK;
 }
 
@@ -374,8 +428,9 @@ int fk_op_pa_data(fk_op* op, double* host_out) {
   if (op == nullptr || host_out == nullptr) return fail(FK_EINVAL, "null argument");
   if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
   DeviceGuard g(op->device);
-  const int64_t n = op->nel * op->npa * op->q * op->q * op->q;
-  FK_CUDA(cudaMemcpyAsync(host_out, op->pa, sizeof(double) * n, cudaMemcpyDeviceToHost, op->stream));
+  const size_t row = sizeof(double) * op->npa * op->q * op->q * op->q;
+  FK_CUDA(cudaMemcpy2DAsync(host_out, row, op->pa, sizeof(double) * op->ps, row, op->nel,
+                            cudaMemcpyDeviceToHost, op->stream));
   FK_CUDA(cudaStreamSynchronize(op->stream));
   return FK_OK;
 }

@@ -16,7 +16,7 @@ using LaunchFn = void (*)(const OpView&, const double* x, double* y, int blocks,
 using DiagFn = void (*)(const OpView&, double* diag, int64_t nel, int blocks, cudaStream_t s);
 
 struct KernelEntry {
-  int nc = 0, d = 0, q = 0, variant = 0;
+  int nc = 0, d = 0, q = 0, variant = 0, cfg = 0;
   int E = 0, T = 0;
   size_t smem = 0;
   const void* func = nullptr;
@@ -29,9 +29,16 @@ struct OpView {
   const double* G;
   const int* gids;
   const double* pa;
-  const unsigned char* mask;
+  const uint32_t* ebits;  // per-element Dirichlet bits (nullptr: none)
   int nel;
 };
+
+// Host mirror of GlobalLayout (pa_common.cuh): padded per-element strides.
+inline int64_t pa_stride(int npa, int q) { return ((int64_t)npa * q * q * q + 1) / 2 * 2; }
+inline int64_t gid_stride(int d) { return ((int64_t)d * d * d + 3) / 4 * 4; }
+inline int64_t bits_stride(int d) { return (((int64_t)d * d * d + 31) / 32 + 3) / 4 * 4; }
+
+const KernelEntry* find_kernel_cfg(int nc, int d, int q, int variant, int cfg);
 
 void register_kernels(std::vector<KernelEntry>& out);  // pa_instances*.cu
 const KernelEntry* find_kernel(int nc, int d, int q, int variant);
@@ -62,6 +69,9 @@ struct fk_op {
   int* gids = nullptr;
   double* pa = nullptr;
   unsigned char* mask = nullptr;
+  uint32_t* ebits = nullptr;
+  int64_t ps = 0, gs = 0, ms = 0;  // padded strides (doubles, ints, words)
+  int cfg = -1;                    // launch-geometry override (FK_CFG)
   int* ess = nullptr;
   int64_t n_ess = 0;
   // host staging for fk_op_apply_host

@@ -12,17 +12,41 @@ namespace fk {
 // local element e = ex + nx*(ey + ny*ez_l), local node l = i + d*(j + d*k):
 //   id = (ex*p + i) + npx*((ey*p + j) + npy*(ez_l*p + k))      (slab-local)
 // The slab-local id plus dof_offset = z0*p*npx*npy is the reference's global id.
+// Rows are padded to gs int32 (16-byte multiples for the bulk copies);
+// padding entries hold a valid id (0) and are never used.
 __global__ void restriction_kernel(int* __restrict__ gids, int nx, int ny, int nzl, int p,
-                                   int64_t npx, int64_t npy) {
+                                   int64_t npx, int64_t npy, int64_t gs) {
   const int d = p + 1, d3 = d * d * d;
-  const int64_t total = (int64_t)nx * ny * nzl * d3;
+  const int64_t total = (int64_t)nx * ny * nzl * gs;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = t / d3;
-    const int l = (int)(t - e * d3);
+    const int64_t e = t / gs;
+    const int l = (int)(t - e * gs);
+    if (l >= d3) {
+      gids[t] = 0;
+      continue;
+    }
     const int i = l % d, j = (l / d) % d, k = l / (d * d);
     const int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / ((int64_t)nx * ny);
     gids[t] = (int)((ex * p + i) + npx * ((ey * p + j) + npy * (ez * p + k)));
+  }
+}
+
+// Per-element Dirichlet bits: bit l of element e set iff its node l is essential.
+__global__ void ebits_kernel(uint32_t* __restrict__ bits, const int* __restrict__ gids,
+                             const unsigned char* __restrict__ mask, int64_t nel, int d3,
+                             int64_t gs, int64_t ms) {
+  const int64_t total = nel * ms;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / ms;
+    const int w = (int)(t - e * ms);
+    uint32_t v = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int l = w * 32 + b;
+      if (l < d3 && mask[gids[e * gs + l]]) v |= 1u << b;
+    }
+    bits[t] = v;
   }
 }
 
@@ -33,7 +57,7 @@ __global__ void restriction_kernel(int* __restrict__ gids, int nx, int ny, int n
 //        (00, 01, 02, 11, 12, 22); on the axis-aligned box the off-diagonal
 //        components are zero and D_ss = wdet * (jinv_s * jinv_s).
 // Layout: pa[e][comp][qp], qp = a + q*(b + q*c) (x fastest), element-major.
-__global__ void pa_data_kernel(double* __restrict__ pa, int64_t nel, int q, int npa,
+__global__ void pa_data_kernel(double* __restrict__ pa, int64_t nel, int q, int npa, int64_t ps,
                                const double* __restrict__ w, double detj, double ji0, double ji1,
                                double ji2) {
   const int q3 = q * q * q;
@@ -45,7 +69,8 @@ __global__ void pa_data_kernel(double* __restrict__ pa, int64_t nel, int q, int 
     const int a = qp % q, b = (qp / q) % q, c = qp / (q * q);
     const double w3 = w[c] * (w[b] * w[a]);
     const double wdet = w3 * detj;
-    double* o = pa + e * npa * q3 + qp;
+    double* o = pa + e * ps + qp;
+    if (qp == 0 && ps > (int64_t)npa * q3) pa[e * ps + npa * q3] = 0.0;  // stride padding
     if (npa == 1) {
       o[0] = wdet;
     } else {

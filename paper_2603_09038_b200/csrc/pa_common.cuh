@@ -60,6 +60,18 @@ struct LineLayout {
   }
 };
 
+// Global (HBM) layout strides per element, padded so every per-batch range
+// is a 16-byte multiple (cp.async.bulk granularity).  Host code mirrors
+// these in fk_api.cu (pa_stride / gid_stride / bits_stride).
+template <int D, int Q, int NC>
+struct GlobalLayout {
+  static constexpr int NPA = (NC == 3) ? 6 : 1;
+  static constexpr int PS = ((NPA * Q * Q * Q + 1) / 2) * 2;  // doubles of PA data per element
+  static constexpr int GS = ((D * D * D + 3) / 4) * 4;        // int32 gather ids per element
+  static constexpr int MW = (D * D * D + 31) / 32;            // Dirichlet bit words per element
+  static constexpr int MS = ((MW + 3) / 4) * 4;               // padded
+};
+
 // L2 bulk prefetch (sm_90+): one instruction moves a contiguous range of the
 // next batch's PA data toward L2 so the later per-thread loads hit L2.
 __device__ __forceinline__ void prefetch_l2(const void* ptr, uint32_t bytes) {

@@ -1,96 +1,100 @@
-// pa_dfma.cuh — fused BP1/BP3 PA apply, register-blocked FP64-FMA ("line") variant.
+// pa_dfma.cuh — contraction stages of the fused PA apply, register-blocked
+// FP64-FMA ("line") variant.  Plugs into pa_pipe.cuh.
 //
-// One persistent CTA processes batches of E elements.  Per batch:
-//
-//   gather   x[gid] -> X (smem), gids kept in smem for the scatter
-//            (Restriction.gather, feklab/mesh.py:130-131)
-//   stage A  contract x: thread per line (j,k): B x, G x           (tensor.py:177-210)
+//   stage A  contract x: thread per line (j,k): B x, G x       (tensor.py:177-210)
 //   stage B  contract y: thread per line (k,a): 3 component chains
 //   stage C  contract z, apply D (6-comp symmetric, BP3; w|J| BP1),
 //            transposed z — all in registers for line (a,b)
 //   stage D  transposed y: thread per line (a,k)
-//   stage E  transposed x: thread per line (j,k), atomic scatter-add to y
+//   stage E  transposed x: thread per line (j,k) + atomic scatter-add
 //            (Restriction.scatter_add, feklab/mesh.py:133-137)
 //
 // MFEM-style stage sharing: BP3 costs 2(4qd^3+6q^2d^2+6q^3d)+15q^3 flops per
 // element instead of the reference's three independent chains
 // (apply_gradient_3d, tensor.py:244-260).  Each thread keeps its line in
-// registers and every FMA takes its basis entry from the constant bank
-// (kernel parameter), so one 8-byte shared load feeds q (or 2q, 3q) FMAs.
+// registers; one 8-byte shared load of the line feeds q (or 2q, 3q) FMAs.
+//
+// Basis tables: sm_100a ptxas turns every double kernel-parameter operand
+// into LDCU + uniform-register traffic and, when it hoists the 2qd table
+// entries out of the persistent loop, spills the uniform register file
+// (measured: ~1000 of 2000 warp instructions per element were R2UR / IMAD /
+// LDCU moves).  The tables therefore live in shared memory as 16-byte-aligned
+// rows (B[a][*], G[a][*] and the transposes) and each row is read with
+// LDS.128 broadcasts right where it is used (__syncthreads between stages
+// keeps the compiler from hoisting them): 0.5 load per table entry, no
+// register pressure from the tables.
 #pragma once
 
 #include "pa_common.cuh"
 
 namespace fk {
 
-template <int D, int Q, int NC, int E, int T>
-__global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tables<D, Q> tb,
-                                                    const double* __restrict__ x,
-                                                    double* __restrict__ y,
-                                                    const int* __restrict__ gids,
-                                                    const double* __restrict__ pa,
-                                                    const unsigned char* __restrict__ mask,
-                                                    int nel) {
+template <int N>
+__device__ __forceinline__ void ld_row(const double* __restrict__ p, double (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i + 1 < N; i += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(p + i);
+    r[i] = v.x;
+    r[i + 1] = v.y;
+  }
+  if constexpr (N & 1) r[N - 1] = p[N - 1];
+}
+
+template <int D, int Q, int NC, int E_, int T_>
+struct DfmaBody {
   using L = LineLayout<D, Q, NC>;
-  constexpr int D3 = L::D3, Q3 = L::Q3, NPA = L::NPA;
-  constexpr int LS = L::LS, LQ = L::LQ, P0 = L::P0, P1 = L::P1;
-  extern __shared__ __align__(16) double smem[];
-  double* s0 = smem;
-  double* s1 = smem + E * P0;
-  int* sg = reinterpret_cast<int*>(s1 + E * P1);
+  using G = GlobalLayout<D, Q, NC>;
+  static constexpr int LS = L::LS, LQ = L::LQ, P0 = L::P0, P1 = L::P1, Q3 = L::Q3;
+  static constexpr int XS = D * D * LS;
+  static constexpr int DP = D + (D & 1), QP = Q + (Q & 1);  // 16-byte row pitch
+  // smem table offsets (doubles): B[a][i], G[a][i] rows of D; Bt[i][a], Gt[i][a] rows of Q
+  static constexpr int TB = 0, TG = TB + Q * DP, TBT = TG + Q * DP, TGT = TBT + D * QP;
+  static constexpr int E = E_, T = T_, EXTRA = TGT + D * QP;
 
-  const int nbatch = (nel + E - 1) / E;
-  const size_t pa_total = (size_t)nel * NPA * Q3;
-  if (threadIdx.x == 0 && blockIdx.x < nbatch)
-    prefetch_range_l2(pa, (size_t)blockIdx.x * E * NPA * Q3, (size_t)E * NPA * Q3, pa_total);
-
-  for (int batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
-    const int e0 = batch * E;
-    if (threadIdx.x == 0) {
-      const int nb = batch + gridDim.x;
-      if (nb < nbatch) prefetch_range_l2(pa, (size_t)nb * E * NPA * Q3, (size_t)E * NPA * Q3, pa_total);
+  __device__ static void init(const Tables<D, Q>& tb, double* t) {
+    for (int n = threadIdx.x; n < Q * D; n += T) {
+      const int a = n / D, i = n % D;
+      t[TB + a * DP + i] = tb.B[n];
+      t[TG + a * DP + i] = tb.G[n];
+      t[TBT + i * QP + a] = tb.B[n];
+      t[TGT + i * QP + a] = tb.G[n];
     }
-    // ---- gather -------------------------------------------------------
-    for (int t = threadIdx.x; t < E * D3; t += T) {
-      const int e = t / D3, l = t - e * D3;
-      int gid = -1;
-      double v = 0.0;
-      if (e0 + e < nel) {
-        gid = __ldg(gids + (size_t)e0 * D3 + t);
-        v = __ldg(x + gid);
-        if (mask != nullptr && __ldg(mask + gid)) v = 0.0;
-      }
-      sg[t] = gid;
-      s0[e * P0 + (l / D) * LS + (l % D)] = v;
-    }
-    __syncthreads();
+  }
 
-    // ---- stage A: contract x (i -> a); line v = j + D*k ----------------
-    for (int t = threadIdx.x; t < E * D * D; t += T) {
+  // X [v=(j,k)][i] -> T1 [s][a][k][j]
+  __device__ __forceinline__ static void stage_a(const Tables<D, Q>&, const double* xb, double* s1,
+                                                 int ne, const double* tab) {
+    for (int t = threadIdx.x; t < ne * D * D; t += T) {
       const int e = t / (D * D), v = t - e * (D * D);
-      const double* in = s0 + e * P0 + v * LS;
+      const double* in = xb + e * XS + v * LS;
       double xr[D];
 #pragma unroll
       for (int i = 0; i < D; ++i) xr[i] = in[i];
       double* o = s1 + e * P1 + (v / D) * LS + (v % D);
 #pragma unroll
       for (int a = 0; a < Q; ++a) {
-        double bx = tb.B[a * D] * xr[0];
+        double br[D];
+        ld_row(tab + TB + a * DP, br);
+        double bx = br[0] * xr[0];
 #pragma unroll
-        for (int i = 1; i < D; ++i) bx = fma(tb.B[a * D + i], xr[i], bx);
+        for (int i = 1; i < D; ++i) bx = fma(br[i], xr[i], bx);
         o[a * D * LS] = bx;
         if constexpr (NC == 3) {
-          double gx = tb.G[a * D] * xr[0];
+          double gr[D];
+          ld_row(tab + TG + a * DP, gr);
+          double gx = gr[0] * xr[0];
 #pragma unroll
-          for (int i = 1; i < D; ++i) gx = fma(tb.G[a * D + i], xr[i], gx);
+          for (int i = 1; i < D; ++i) gx = fma(gr[i], xr[i], gx);
           o[Q * D * LS + a * D * LS] = gx;
         }
       }
     }
-    __syncthreads();
+  }
 
-    // ---- stage B: contract y (j -> b); line u = k + D*a ----------------
-    for (int t = threadIdx.x; t < E * D * Q; t += T) {
+  // T1 [s][a][k][j] (line u = k + D a) -> T2 [s][b][a][k]
+  __device__ __forceinline__ static void stage_b(const Tables<D, Q>&, const double* s1, double* s0,
+                                                 int ne, const double* tab) {
+    for (int t = threadIdx.x; t < ne * D * Q; t += T) {
       const int e = t / (D * Q), u = t - e * (D * Q);
       const double* in = s1 + e * P1 + u * LS;
       double bx[D];
@@ -104,14 +108,17 @@ __global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tabl
         for (int j = 0; j < D; ++j) gx[j] = in[Q * D * LS + j];
 #pragma unroll
         for (int b = 0; b < Q; ++b) {
-          double c0 = tb.B[b * D] * gx[0];
-          double c1 = tb.G[b * D] * bx[0];
-          double c2 = tb.B[b * D] * bx[0];
+          double br[D], gr[D];
+          ld_row(tab + TB + b * DP, br);
+          ld_row(tab + TG + b * DP, gr);
+          double c0 = br[0] * gx[0];
+          double c1 = gr[0] * bx[0];
+          double c2 = br[0] * bx[0];
 #pragma unroll
           for (int j = 1; j < D; ++j) {
-            c0 = fma(tb.B[b * D + j], gx[j], c0);
-            c1 = fma(tb.G[b * D + j], bx[j], c1);
-            c2 = fma(tb.B[b * D + j], bx[j], c2);
+            c0 = fma(br[j], gx[j], c0);
+            c1 = fma(gr[j], bx[j], c1);
+            c2 = fma(br[j], bx[j], c2);
           }
           o[b * Q * LS] = c0;
           o[Q * Q * LS + b * Q * LS] = c1;
@@ -120,21 +127,25 @@ __global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tabl
       } else {
 #pragma unroll
         for (int b = 0; b < Q; ++b) {
-          double c = tb.B[b * D] * bx[0];
+          double br[D];
+          ld_row(tab + TB + b * DP, br);
+          double c = br[0] * bx[0];
 #pragma unroll
-          for (int j = 1; j < D; ++j) c = fma(tb.B[b * D + j], bx[j], c);
+          for (int j = 1; j < D; ++j) c = fma(br[j], bx[j], c);
           o[b * Q * LS] = c;
         }
       }
     }
-    __syncthreads();
+  }
 
-    // ---- stage C: contract z, D, transposed z; line r = a + Q*b ---------
-    for (int t = threadIdx.x; t < E * Q * Q; t += T) {
+  // T2 [s][b][a][k] (line r = a + Q b) + D -> W [s][k][a][b]
+  __device__ __forceinline__ static void stage_c(const Tables<D, Q>&, const double* s0,
+                                                 const double* db, double* s1, int ne,
+                                                 const double* tab) {
+    for (int t = threadIdx.x; t < ne * Q * Q; t += T) {
       const int e = t / (Q * Q), r = t - e * (Q * Q);
-      const bool valid = (e0 + e) < nel;
       const double* in = s0 + e * P0 + r * LS;
-      const double* pe = pa + ((size_t)(e0 + e) * NPA * Q3 + r);
+      const double* pe = db + e * G::PS + r;
       const int a = r % Q, b = r / Q;
       double* o = s1 + e * P1 + a * LQ + b;
       if constexpr (NC == 3) {
@@ -150,33 +161,29 @@ __global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tabl
         }
 #pragma unroll
         for (int c = 0; c < Q; ++c) {
-          double g0 = tb.B[c * D] * t0[0];
-          double g1 = tb.B[c * D] * t1[0];
-          double g2 = tb.G[c * D] * t2[0];
+          double br[D], gr[D];
+          ld_row(tab + TB + c * DP, br);
+          ld_row(tab + TG + c * DP, gr);
+          double g0 = br[0] * t0[0];
+          double g1 = br[0] * t1[0];
+          double g2 = gr[0] * t2[0];
 #pragma unroll
           for (int k = 1; k < D; ++k) {
-            g0 = fma(tb.B[c * D + k], t0[k], g0);
-            g1 = fma(tb.B[c * D + k], t1[k], g1);
-            g2 = fma(tb.G[c * D + k], t2[k], g2);
+            g0 = fma(br[k], t0[k], g0);
+            g1 = fma(br[k], t1[k], g1);
+            g2 = fma(gr[k], t2[k], g2);
           }
-          double d00 = 0, d01 = 0, d02 = 0, d11 = 0, d12 = 0, d22 = 0;
-          if (valid) {
-            const double* pc = pe + c * Q * Q;
-            d00 = ld_stream(pc + 0 * Q3);
-            d01 = ld_stream(pc + 1 * Q3);
-            d02 = ld_stream(pc + 2 * Q3);
-            d11 = ld_stream(pc + 3 * Q3);
-            d12 = ld_stream(pc + 4 * Q3);
-            d22 = ld_stream(pc + 5 * Q3);
-          }
+          const double* pc = pe + c * Q * Q;
+          const double d00 = pc[0 * Q3], d01 = pc[1 * Q3], d02 = pc[2 * Q3];
+          const double d11 = pc[3 * Q3], d12 = pc[4 * Q3], d22 = pc[5 * Q3];
           const double o0 = fma(d02, g2, fma(d01, g1, d00 * g0));
           const double o1 = fma(d12, g2, fma(d11, g1, d01 * g0));
           const double o2 = fma(d22, g2, fma(d12, g1, d02 * g0));
 #pragma unroll
           for (int k = 0; k < D; ++k) {
-            w0[k] = fma(tb.B[c * D + k], o0, w0[k]);
-            w1[k] = fma(tb.B[c * D + k], o1, w1[k]);
-            w2[k] = fma(tb.G[c * D + k], o2, w2[k]);
+            w0[k] = fma(br[k], o0, w0[k]);
+            w1[k] = fma(br[k], o1, w1[k]);
+            w2[k] = fma(gr[k], o2, w2[k]);
           }
         }
 #pragma unroll
@@ -194,22 +201,25 @@ __global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tabl
         }
 #pragma unroll
         for (int c = 0; c < Q; ++c) {
-          double g = tb.B[c * D] * tt[0];
+          double br[D];
+          ld_row(tab + TB + c * DP, br);
+          double g = br[0] * tt[0];
 #pragma unroll
-          for (int k = 1; k < D; ++k) g = fma(tb.B[c * D + k], tt[k], g);
-          const double dd = valid ? ld_stream(pe + c * Q * Q) : 0.0;
-          const double oo = dd * g;
+          for (int k = 1; k < D; ++k) g = fma(br[k], tt[k], g);
+          const double oo = pe[c * Q * Q] * g;
 #pragma unroll
-          for (int k = 0; k < D; ++k) w[k] = fma(tb.B[c * D + k], oo, w[k]);
+          for (int k = 0; k < D; ++k) w[k] = fma(br[k], oo, w[k]);
         }
 #pragma unroll
         for (int k = 0; k < D; ++k) o[k * Q * LQ] = w[k];
       }
     }
-    __syncthreads();
+  }
 
-    // ---- stage D: transposed y (b -> j); line u = a + Q*k ---------------
-    for (int t = threadIdx.x; t < E * Q * D; t += T) {
+  // W [s][k][a][b] (line u = a + Q k) -> R [s][k][j][a]
+  __device__ __forceinline__ static void stage_d(const Tables<D, Q>&, const double* s1, double* s0,
+                                                 int ne, const double* tab) {
+    for (int t = threadIdx.x; t < ne * Q * D; t += T) {
       const int e = t / (Q * D), u = t - e * (Q * D);
       const double* in = s1 + e * P1 + u * LQ;
       const int a = u % Q, k = u / Q;
@@ -224,15 +234,18 @@ __global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tabl
         }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-          double rg = tb.B[j] * w0[0];
-          double rb = tb.G[j] * w1[0];
+          double bt[Q], gt[Q];
+          ld_row(tab + TBT + j * QP, bt);
+          ld_row(tab + TGT + j * QP, gt);
+          double rg = bt[0] * w0[0];
+          double rb = gt[0] * w1[0];
 #pragma unroll
           for (int b = 1; b < Q; ++b) {
-            rg = fma(tb.B[b * D + j], w0[b], rg);
-            rb = fma(tb.G[b * D + j], w1[b], rb);
+            rg = fma(bt[b], w0[b], rg);
+            rb = fma(gt[b], w1[b], rb);
           }
 #pragma unroll
-          for (int b = 0; b < Q; ++b) rb = fma(tb.B[b * D + j], w2[b], rb);
+          for (int b = 0; b < Q; ++b) rb = fma(bt[b], w2[b], rb);
           o[j * LQ] = rg;
           o[D * D * LQ + j * LQ] = rb;
         }
@@ -242,20 +255,25 @@ __global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tabl
         for (int b = 0; b < Q; ++b) w[b] = in[b];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-          double rr = tb.B[j] * w[0];
+          double bt[Q];
+          ld_row(tab + TBT + j * QP, bt);
+          double rr = bt[0] * w[0];
 #pragma unroll
-          for (int b = 1; b < Q; ++b) rr = fma(tb.B[b * D + j], w[b], rr);
+          for (int b = 1; b < Q; ++b) rr = fma(bt[b], w[b], rr);
           o[j * LQ] = rr;
         }
       }
     }
-    __syncthreads();
+  }
 
-    // ---- stage E: transposed x (a -> i) + scatter; line v = j + D*k ------
-    for (int t = threadIdx.x; t < E * D * D; t += T) {
+  // R [s][k][j][a] (line v = j + D k) -> y (atomic scatter-add)
+  __device__ __forceinline__ static void stage_e(const Tables<D, Q>&, const double* s0,
+                                                 const int* gslot, double* y, int ne,
+                                                 const double* tab) {
+    for (int t = threadIdx.x; t < ne * D * D; t += T) {
       const int e = t / (D * D), v = t - e * (D * D);
       const double* in = s0 + e * P0 + v * LQ;
-      const int* g = sg + e * D3 + v * D;
+      const int* g = gslot + e * G::GS + v * D;
       if constexpr (NC == 3) {
         double rg[Q], rb[Q];
 #pragma unroll
@@ -265,13 +283,15 @@ __global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tabl
         }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-          double acc = tb.G[i] * rg[0];
+          double bt[Q], gt[Q];
+          ld_row(tab + TBT + i * QP, bt);
+          ld_row(tab + TGT + i * QP, gt);
+          double acc = gt[0] * rg[0];
 #pragma unroll
-          for (int a = 1; a < Q; ++a) acc = fma(tb.G[a * D + i], rg[a], acc);
+          for (int a = 1; a < Q; ++a) acc = fma(gt[a], rg[a], acc);
 #pragma unroll
-          for (int a = 0; a < Q; ++a) acc = fma(tb.B[a * D + i], rb[a], acc);
-          const int gid = g[i];
-          if (gid >= 0) atomicAdd(y + gid, acc);
+          for (int a = 0; a < Q; ++a) acc = fma(bt[a], rb[a], acc);
+          atomicAdd(y + g[i], acc);
         }
       } else {
         double rr[Q];
@@ -279,16 +299,16 @@ __global__ void __launch_bounds__(T) pa_dfma_kernel(const __grid_constant__ Tabl
         for (int a = 0; a < Q; ++a) rr[a] = in[a];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-          double acc = tb.B[i] * rr[0];
+          double bt[Q];
+          ld_row(tab + TBT + i * QP, bt);
+          double acc = bt[0] * rr[0];
 #pragma unroll
-          for (int a = 1; a < Q; ++a) acc = fma(tb.B[a * D + i], rr[a], acc);
-          const int gid = g[i];
-          if (gid >= 0) atomicAdd(y + gid, acc);
+          for (int a = 1; a < Q; ++a) acc = fma(bt[a], rr[a], acc);
+          atomicAdd(y + g[i], acc);
         }
       }
     }
-    __syncthreads();
   }
-}
+};
 
 }  // namespace fk

@@ -17,14 +17,14 @@ __global__ void diagonal_kernel(const __grid_constant__ Tables<D, Q> tb,
                                 double* __restrict__ diag, const int* __restrict__ gids,
                                 const double* __restrict__ pa, int64_t nel) {
   constexpr int D3 = D * D * D, Q3 = Q * Q * Q;
-  constexpr int NPA = (NC == 3) ? 6 : 1;
+  using G = GlobalLayout<D, Q, NC>;
   const int64_t total = nel * D3;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = t / D3;
     const int l = (int)(t - e * D3);
     const int i = l % D, j = (l / D) % D, k = l / (D * D);
-    const double* pe = pa + e * NPA * Q3;
+    const double* pe = pa + e * G::PS;
     double acc = 0.0;
     for (int c = 0; c < Q; ++c) {
       const double bc = tb.B[c * D + k], gc = tb.G[c * D + k];
@@ -46,7 +46,7 @@ __global__ void diagonal_kernel(const __grid_constant__ Tables<D, Q> tb,
         }
       }
     }
-    atomicAdd(diag + gids[t], acc);
+    atomicAdd(diag + gids[e * G::GS + l], acc);
   }
 }
 

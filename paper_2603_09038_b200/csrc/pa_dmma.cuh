@@ -1,17 +1,17 @@
-// pa_dmma.cuh — fused BP1/BP3 PA apply with every 1D contraction on the FP64
-// tensor cores: warp-level mma.sync.aligned.m8n8k4.row.col.f64 (DMMA.8x8x4,
-// the only FP64 tensor instruction sm_100a has; tcgen05 has no f64 kind).
+// pa_dmma.cuh — contraction stages of the fused PA apply on the FP64 tensor
+// cores: warp-level mma.sync.aligned.m8n8k4.row.col.f64 (SASS DMMA.8x8x4, the
+// only FP64 tensor instruction sm_100a has; tcgen05 has no f64 kind).
+// Plugs into pa_pipe.cuh.
 //
-// Same dataflow and shared-memory layouts as pa_dfma.cuh; each stage is a
-// batched small GEMM  C[m][n] = sum_k A[m][k] * Bop[k][n]  with
-//   m = (element, line) rows of all E elements of the CTA (batched along M,
-//       removing the M-padding waste of per-element tiles),
-//   k = the contracted 1D index (K-concatenated where two legs sum),
-//   n = the new 1D index (N-concatenated where one input feeds B and G).
+// Each stage is a batched small GEMM  C[m][n] = sum_k A[m][k] * Bop[k][n]:
+//   m = (element, line) rows of all E elements of the CTA (batching along M
+//       removes the M-padding waste of per-element tiles),
+//   k = the contracted 1D index (K-concatenated where two legs are summed),
+//   n = the new 1D index (N-concatenated where one input feeds both B and G).
 // Fragment semantics follow the reference's emulation (feklab/mma.py:70-143):
-// lane L holds A(L/4, L%4), B(L%4, L/4), C(L/4, 2(L%4)+{0,1}); padded
-// fragment entries are zero (mma.py:283-296).  The B operands (basis tables)
-// are pre-swizzled per lane into shared memory once per CTA.
+// lane L holds A(L/4, L%4), B(L%4, L/4), C(L/4, 2(L%4)+{0,1}); padded entries
+// are zero (mma.py:283-296).  The B operands (basis tables) are pre-swizzled
+// per lane into shared memory once per CTA.
 //
 // Stage C keeps its accumulators in registers: the three gradient components
 // land in identical C-fragment positions, D is applied in registers, and the
@@ -31,29 +31,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 
 constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
 
-template <int D, int Q, int NC>
-struct DmmaConfig {
-  using L = LineLayout<D, Q, NC>;
-  static constexpr int E = cmax(1, 256 / (Q * Q));
-  static constexpr int T = 256;
-  static constexpr int NW = T / 32;
-  static constexpr int KD = cdiv(D, 4), KQ = cdiv(Q, 4), K2Q = cdiv(2 * Q, 4);
-  static constexpr int NQ = cdiv(Q, 8), N2Q = cdiv(2 * Q, 8), ND = cdiv(D, 8);
-  // fragment tables (doubles, 32 per (ntile, kstep))
-  static constexpr int F_A = 0;                                        // [B;G] or B, K=D
-  static constexpr int F_B1 = F_A + (NC == 3 ? N2Q : NQ) * KD * 32;    // [G;B] or B, K=D
-  static constexpr int F_CB = F_B1 + (NC == 3 ? N2Q : NQ) * KD * 32;   // B, K=D
-  static constexpr int F_CG = F_CB + NQ * KD * 32;                     // G, K=D
-  static constexpr int F_TB = F_CG + NQ * KD * 32;                     // B^T, K=Q
-  static constexpr int F_TG = F_TB + ND * KQ * 32;                     // G^T, K=Q
-  static constexpr int F_GB = F_TG + ND * KQ * 32;                     // [G^T;B^T], K=2Q
-  static constexpr int F_END = F_GB + ND * K2Q * 32;
-  static constexpr size_t smem_bytes() {
-    return sizeof(double) * ((size_t)E * (L::P0 + L::P1) + F_END) + sizeof(int) * (size_t)E * L::D3;
-  }
-};
-
-// Generic batched stage: rows [0, rows) of 8-row tiles distributed over warps.
+// Generic batched stage: 8-row tiles of rows [0, rows) distributed over warps.
 // aval(m, k) returns A[m][k] (0 beyond K); store(m, n, c0, c1) writes C[m][n], C[m][n+1].
 template <int NW, int KS, int NT, typename AVal, typename Store>
 __device__ __forceinline__ void dmma_stage(int rows, const double* __restrict__ frag, AVal aval,
@@ -79,287 +57,258 @@ __device__ __forceinline__ void dmma_stage(int rows, const double* __restrict__ 
   }
 }
 
-template <int D, int Q, int NC>
-__global__ void __launch_bounds__(DmmaConfig<D, Q, NC>::T) pa_dmma_kernel(
-    const __grid_constant__ Tables<D, Q> tb, const double* __restrict__ x, double* __restrict__ y,
-    const int* __restrict__ gids, const double* __restrict__ pa,
-    const unsigned char* __restrict__ mask, int nel) {
-  using K = DmmaConfig<D, Q, NC>;
+template <int D, int Q, int NC, int E_, int T_>
+struct DmmaBody {
   using L = LineLayout<D, Q, NC>;
-  constexpr int E = K::E, T = K::T, NW = K::NW;
-  constexpr int D3 = L::D3, Q3 = L::Q3, NPA = L::NPA;
-  constexpr int LS = L::LS, LQ = L::LQ, P0 = L::P0, P1 = L::P1;
-  extern __shared__ __align__(16) double smem[];
-  double* s0 = smem;
-  double* s1 = s0 + E * P0;
-  double* fr = s1 + E * P1;
-  int* sg = reinterpret_cast<int*>(fr + K::F_END);
-  const int lane = threadIdx.x & 31;
+  using G = GlobalLayout<D, Q, NC>;
+  static constexpr int E = E_, T = T_, NW = T_ / 32;
+  static constexpr int LS = L::LS, LQ = L::LQ, P0 = L::P0, P1 = L::P1, Q3 = L::Q3, D3 = L::D3;
+  static constexpr int XS = D * D * LS;
+  static constexpr int KD = cdiv(D, 4), KQ = cdiv(Q, 4), K2Q = cdiv(2 * Q, 4);
+  static constexpr int NQ = cdiv(Q, 8), N2Q = cdiv(2 * Q, 8), ND = cdiv(D, 8);
+  static constexpr int NA = (NC == 3) ? N2Q : NQ;
+  // per-lane fragment tables in smem (doubles; 32 per (ntile, kstep))
+  static constexpr int F_A = 0;                   // [B;G] (BP1: B), K = D
+  static constexpr int F_B1 = F_A + NA * KD * 32;  // [G;B] (BP1: B), K = D
+  static constexpr int F_CB = F_B1 + NA * KD * 32; // B, K = D
+  static constexpr int F_CG = F_CB + NQ * KD * 32; // G, K = D
+  static constexpr int F_TB = F_CG + NQ * KD * 32; // B^T, K = Q
+  static constexpr int F_TG = F_TB + ND * KQ * 32; // G^T, K = Q
+  static constexpr int F_GB = F_TG + ND * KQ * 32; // [G^T;B^T], K = 2Q
+  static constexpr int EXTRA = F_GB + ND * K2Q * 32;
 
-  // ---- per-lane B-operand fragments: frag(nt, ks, L) = Bop[4ks + L%4][8nt + L/4]
-  auto fill = [&](int off, int NT, int KS, auto bop) {
-    for (int t = threadIdx.x; t < NT * KS * 32; t += T) {
-      const int l = t & 31, ks = (t >> 5) % KS, nt = (t >> 5) / KS;
+  template <typename Bop>
+  __device__ static void fill(double* fr, int off, int ntiles, int ksteps, Bop bop) {
+    for (int t = threadIdx.x; t < ntiles * ksteps * 32; t += T) {
+      const int l = t & 31, ks = (t >> 5) % ksteps, nt = (t >> 5) / ksteps;
       fr[off + t] = bop(4 * ks + (l & 3), 8 * nt + (l >> 2));
     }
-  };
-  if constexpr (NC == 3) {
-    fill(K::F_A, K::N2Q, K::KD, [&](int k, int n) {
-      return k >= D ? 0.0 : n < Q ? tb.B[n * D + k] : n < 2 * Q ? tb.G[(n - Q) * D + k] : 0.0;
-    });
-    fill(K::F_B1, K::N2Q, K::KD, [&](int k, int n) {
-      return k >= D ? 0.0 : n < Q ? tb.G[n * D + k] : n < 2 * Q ? tb.B[(n - Q) * D + k] : 0.0;
-    });
-  } else {
-    fill(K::F_A, K::NQ, K::KD, [&](int k, int n) { return (k < D && n < Q) ? tb.B[n * D + k] : 0.0; });
-    fill(K::F_B1, K::NQ, K::KD, [&](int k, int n) { return (k < D && n < Q) ? tb.B[n * D + k] : 0.0; });
   }
-  fill(K::F_CB, K::NQ, K::KD, [&](int k, int n) { return (k < D && n < Q) ? tb.B[n * D + k] : 0.0; });
-  fill(K::F_CG, K::NQ, K::KD, [&](int k, int n) { return (k < D && n < Q) ? tb.G[n * D + k] : 0.0; });
-  fill(K::F_TB, K::ND, K::KQ, [&](int k, int n) { return (k < Q && n < D) ? tb.B[k * D + n] : 0.0; });
-  fill(K::F_TG, K::ND, K::KQ, [&](int k, int n) { return (k < Q && n < D) ? tb.G[k * D + n] : 0.0; });
-  fill(K::F_GB, K::ND, K::K2Q, [&](int k, int n) {
-    return n >= D ? 0.0 : k < Q ? tb.G[k * D + n] : k < 2 * Q ? tb.B[(k - Q) * D + n] : 0.0;
-  });
 
-  const int nbatch = (nel + E - 1) / E;
-  const size_t pa_total = (size_t)nel * NPA * Q3;
-  if (threadIdx.x == 0 && blockIdx.x < nbatch)
-    prefetch_range_l2(pa, (size_t)blockIdx.x * E * NPA * Q3, (size_t)E * NPA * Q3, pa_total);
-  __syncthreads();
-
-  for (int batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
-    const int e0 = batch * E;
-    const int ne = min(E, nel - e0);
-    if (threadIdx.x == 0) {
-      const int nb = batch + gridDim.x;
-      if (nb < nbatch) prefetch_range_l2(pa, (size_t)nb * E * NPA * Q3, (size_t)E * NPA * Q3, pa_total);
+  // frag(nt, ks, L) = Bop[4ks + L%4][8nt + L/4]
+  __device__ static void init(const Tables<D, Q>& tb, double* fr) {
+    if constexpr (NC == 3) {
+      fill(fr, F_A, NA, KD, [&](int k, int n) {
+        return k >= D ? 0.0 : n < Q ? tb.B[n * D + k] : n < 2 * Q ? tb.G[(n - Q) * D + k] : 0.0;
+      });
+      fill(fr, F_B1, NA, KD, [&](int k, int n) {
+        return k >= D ? 0.0 : n < Q ? tb.G[n * D + k] : n < 2 * Q ? tb.B[(n - Q) * D + k] : 0.0;
+      });
+    } else {
+      fill(fr, F_A, NA, KD, [&](int k, int n) { return (k < D && n < Q) ? tb.B[n * D + k] : 0.0; });
+      fill(fr, F_B1, NA, KD, [&](int k, int n) { return (k < D && n < Q) ? tb.B[n * D + k] : 0.0; });
     }
-    // ---- gather -------------------------------------------------------
-    for (int t = threadIdx.x; t < E * D3; t += T) {
-      const int e = t / D3, l = t - e * D3;
-      int gid = -1;
-      double v = 0.0;
-      if (e < ne) {
-        gid = __ldg(gids + (size_t)e0 * D3 + t);
-        v = __ldg(x + gid);
-        if (mask != nullptr && __ldg(mask + gid)) v = 0.0;
+    fill(fr, F_CB, NQ, KD, [&](int k, int n) { return (k < D && n < Q) ? tb.B[n * D + k] : 0.0; });
+    fill(fr, F_CG, NQ, KD, [&](int k, int n) { return (k < D && n < Q) ? tb.G[n * D + k] : 0.0; });
+    fill(fr, F_TB, ND, KQ, [&](int k, int n) { return (k < Q && n < D) ? tb.B[k * D + n] : 0.0; });
+    fill(fr, F_TG, ND, KQ, [&](int k, int n) { return (k < Q && n < D) ? tb.G[k * D + n] : 0.0; });
+    fill(fr, F_GB, ND, K2Q, [&](int k, int n) {
+      return n >= D ? 0.0 : k < Q ? tb.G[k * D + n] : k < 2 * Q ? tb.B[(k - Q) * D + n] : 0.0;
+    });
+  }
+
+  // rows (e, v = j + D k), K = i, N = [B;G] a  ->  T1 [s][a][k][j]
+  __device__ __forceinline__ static void stage_a(const Tables<D, Q>&, const double* xb, double* s1,
+                                                 int ne, double* fr) {
+    auto aval = [&](int m, int k) -> double {
+      const int e = m / (D * D), v = m - e * (D * D);
+      return k < D ? xb[e * XS + v * LS + k] : 0.0;
+    };
+    auto store = [&](int m, int n, double c0, double c1) {
+      const int e = m / (D * D), v = m - e * (D * D);
+      double* o = s1 + e * P1 + (v / D) * LS + (v % D);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int nn = n + h;
+        const double cv = h ? c1 : c0;
+        if (nn < Q) o[nn * D * LS] = cv;
+        else if (NC == 3 && nn < 2 * Q) o[Q * D * LS + (nn - Q) * D * LS] = cv;
       }
-      sg[t] = gid;
-      s0[e * P0 + (l / D) * LS + (l % D)] = v;
-    }
-    __syncthreads();
+    };
+    dmma_stage<NW, KD, NA>(ne * D * D, fr + F_A, aval, store);
+  }
 
-    // ---- stage A: rows (e, v=j+Dk), K = i, N = [B;G] a -------------------
-    {
-      auto aval = [&](int m, int k) -> double {
-        const int e = m / (D * D), v = m - e * (D * D);
-        return k < D ? s0[e * P0 + v * LS + k] : 0.0;
-      };
-      auto store = [&](int m, int n, double c0, double c1) {
-        const int e = m / (D * D), v = m - e * (D * D);
-        double* o = s1 + e * P1 + (v / D) * LS + (v % D);
+  // rows (e, u = k + D a), K = j  ->  T2 [s][b][a][k]
+  __device__ __forceinline__ static void stage_b(const Tables<D, Q>&, const double* s1, double* s0,
+                                                 int ne, double* fr) {
+    auto store_s = [&](int m, int b, int s, double v) {
+      const int e = m / (D * Q), u = m - e * (D * Q);
+      s0[e * P0 + s * Q * Q * LS + (b * Q + u / D) * LS + (u % D)] = v;
+    };
+    auto abx = [&](int m, int k) -> double {
+      const int e = m / (D * Q), u = m - e * (D * Q);
+      return k < D ? s1[e * P1 + u * LS + k] : 0.0;
+    };
+    auto st0 = [&](int m, int n, double c0, double c1) {
+      if (n < Q) store_s(m, n, 0, c0);
+      if (n + 1 < Q) store_s(m, n + 1, 0, c1);
+    };
+    if constexpr (NC == 3) {
+      // B x -> [G;B]: comp1 = G_y B_x (s=1), comp2 = B_y B_x (s=2)
+      auto st12 = [&](int m, int n, double c0, double c1) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int nn = n + h;
           const double cv = h ? c1 : c0;
-          if (nn < Q) o[nn * D * LS] = cv;
-          else if (NC == 3 && nn < 2 * Q) o[Q * D * LS + (nn - Q) * D * LS] = cv;
+          if (nn < Q) store_s(m, nn, 1, cv);
+          else if (nn < 2 * Q) store_s(m, nn - Q, 2, cv);
         }
       };
-      dmma_stage<NW, K::KD, (NC == 3 ? K::N2Q : K::NQ)>(ne * D * D, fr + K::F_A, aval, store);
-    }
-    __syncthreads();
-
-    // ---- stage B: rows (e, u=k+Da), K = j -------------------------------
-    {
-      auto store_s = [&](int m, int b, int s, double v) {
+      dmma_stage<NW, KD, N2Q>(ne * D * Q, fr + F_B1, abx, st12);
+      // G x -> B: comp0 = B_y G_x (s=0)
+      auto agx = [&](int m, int k) -> double {
         const int e = m / (D * Q), u = m - e * (D * Q);
-        s0[e * P0 + s * Q * Q * LS + (b * Q + u / D) * LS + (u % D)] = v;
+        return k < D ? s1[e * P1 + Q * D * LS + u * LS + k] : 0.0;
       };
-      if constexpr (NC == 3) {
-        // bx -> [G;B]: c1 = G bx (s=1), c2 = B bx (s=2)
-        auto abx = [&](int m, int k) -> double {
-          const int e = m / (D * Q), u = m - e * (D * Q);
-          return k < D ? s1[e * P1 + u * LS + k] : 0.0;
-        };
-        auto st1 = [&](int m, int n, double c0, double c1) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int nn = n + h;
-            const double cv = h ? c1 : c0;
-            if (nn < Q) store_s(m, nn, 1, cv);
-            else if (nn < 2 * Q) store_s(m, nn - Q, 2, cv);
-          }
-        };
-        dmma_stage<NW, K::KD, K::N2Q>(ne * D * Q, fr + K::F_B1, abx, st1);
-        // gx -> B: c0 = B gx (s=0)
-        auto agx = [&](int m, int k) -> double {
-          const int e = m / (D * Q), u = m - e * (D * Q);
-          return k < D ? s1[e * P1 + Q * D * LS + u * LS + k] : 0.0;
-        };
-        auto st0 = [&](int m, int n, double c0, double c1) {
-          if (n < Q) store_s(m, n, 0, c0);
-          if (n + 1 < Q) store_s(m, n + 1, 0, c1);
-        };
-        dmma_stage<NW, K::KD, K::NQ>(ne * D * Q, fr + K::F_CB, agx, st0);
-      } else {
-        auto abx = [&](int m, int k) -> double {
-          const int e = m / (D * Q), u = m - e * (D * Q);
-          return k < D ? s1[e * P1 + u * LS + k] : 0.0;
-        };
-        auto st0 = [&](int m, int n, double c0, double c1) {
-          if (n < Q) store_s(m, n, 0, c0);
-          if (n + 1 < Q) store_s(m, n + 1, 0, c1);
-        };
-        dmma_stage<NW, K::KD, K::NQ>(ne * D * Q, fr + K::F_B1, abx, st0);
-      }
+      dmma_stage<NW, KD, NQ>(ne * D * Q, fr + F_CB, agx, st0);
+    } else {
+      dmma_stage<NW, KD, NQ>(ne * D * Q, fr + F_B1, abx, st0);
     }
-    __syncthreads();
-
-    // ---- stage C: rows (e, r=a+Qb): z-contraction, D, transposed z -------
-    {
-      constexpr int NQ = K::NQ, KD = K::KD, KQ = K::KQ, ND = K::ND;
-      const int warp = threadIdx.x >> 5, rr = lane >> 2, cc = lane & 3;
-      const int rows = ne * Q * Q;
-      for (int m0 = warp * 8; m0 < rows; m0 += NW * 8) {
-        const int m = m0 + rr;
-        const bool ok = m < rows;
-        const int e = ok ? m / (Q * Q) : 0, r = m - e * (Q * Q);
-        double g[NC][NQ][2];
-#pragma unroll
-        for (int s = 0; s < NC; ++s)
-#pragma unroll
-          for (int nt = 0; nt < NQ; ++nt) g[s][nt][0] = g[s][nt][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KD; ++ks) {
-          const int k = ks * 4 + cc;
-#pragma unroll
-          for (int s = 0; s < NC; ++s) {
-            const double a = (ok && k < D) ? s0[e * P0 + s * Q * Q * LS + r * LS + k] : 0.0;
-            const double* f = fr + ((NC == 3 && s == 2) ? K::F_CG : K::F_CB);
-#pragma unroll
-            for (int nt = 0; nt < NQ; ++nt) dmma884(g[s][nt][0], g[s][nt][1], a, f[(nt * KD + ks) * 32 + lane]);
-          }
-        }
-        // pointwise D on the fragments: element (m, c = 8nt + 2cc + h)
-        const double* pe = pa + ((size_t)(e0 + e) * NPA * Q3 + r);
-#pragma unroll
-        for (int nt = 0; nt < NQ; ++nt) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = nt * 8 + 2 * cc + h;
-            if (ok && c < Q) {
-              const double* pc = pe + c * Q * Q;
-              if constexpr (NC == 3) {
-                const double d00 = ld_stream(pc), d01 = ld_stream(pc + Q3), d02 = ld_stream(pc + 2 * Q3);
-                const double d11 = ld_stream(pc + 3 * Q3), d12 = ld_stream(pc + 4 * Q3), d22 = ld_stream(pc + 5 * Q3);
-                const double g0 = g[0][nt][h], g1 = g[1][nt][h], g2 = g[2][nt][h];
-                g[0][nt][h] = fma(d02, g2, fma(d01, g1, d00 * g0));
-                g[1][nt][h] = fma(d12, g2, fma(d11, g1, d01 * g0));
-                g[2][nt][h] = fma(d22, g2, fma(d12, g1, d02 * g0));
-              } else {
-                g[0][nt][h] *= ld_stream(pc);
-              }
-            } else {
-#pragma unroll
-              for (int s = 0; s < NC; ++s) g[s][nt][h] = 0.0;
-            }
-          }
-        }
-        // transposed z: W_s[m][k'] = sum_c Mat_s[c][k'] o_s[m][c]; A from C fragments
-        double w[NC][ND][2];
-#pragma unroll
-        for (int s = 0; s < NC; ++s)
-#pragma unroll
-          for (int nt = 0; nt < ND; ++nt) w[s][nt][0] = w[s][nt][1] = 0.0;
-        const int src = (lane & ~3) + ((lane & 3) >> 1);
-#pragma unroll
-        for (int ks = 0; ks < KQ; ++ks) {
-          const int tile = ks >> 1, sl = src + 2 * (ks & 1);
-#pragma unroll
-          for (int s = 0; s < NC; ++s) {
-            const double v0 = __shfl_sync(0xffffffffu, g[s][tile][0], sl);
-            const double v1 = __shfl_sync(0xffffffffu, g[s][tile][1], sl);
-            const double a = (lane & 1) ? v1 : v0;
-            const double* f = fr + ((NC == 3 && s == 2) ? K::F_TG : K::F_TB);
-#pragma unroll
-            for (int nt = 0; nt < ND; ++nt) dmma884(w[s][nt][0], w[s][nt][1], a, f[(nt * KQ + ks) * 32 + lane]);
-          }
-        }
-        if (ok) {
-          const int a = r % Q, b = r / Q;
-          double* o = s1 + e * P1 + a * LQ + b;
-#pragma unroll
-          for (int nt = 0; nt < ND; ++nt)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int kk = nt * 8 + 2 * cc + h;
-              if (kk < D) {
-#pragma unroll
-                for (int s = 0; s < NC; ++s) o[s * D * Q * LQ + kk * Q * LQ] = w[s][nt][h];
-              }
-            }
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- stage D: rows (e, u=a+Qk), K = b (transposed y) ------------------
-    {
-      auto store_r = [&](int m, int j, int s, double v) {
-        const int e = m / (Q * D), u = m - e * (Q * D);
-        s0[e * P0 + s * D * D * LQ + ((u / Q) * D + j) * LQ + (u % Q)] = v;
-      };
-      auto a0 = [&](int m, int k) -> double {
-        const int e = m / (Q * D), u = m - e * (Q * D);
-        return k < Q ? s1[e * P1 + u * LQ + k] : 0.0;
-      };
-      auto st0 = [&](int m, int n, double c0, double c1) {
-        if (n < D) store_r(m, n, 0, c0);
-        if (n + 1 < D) store_r(m, n + 1, 0, c1);
-      };
-      dmma_stage<NW, K::KQ, K::ND>(ne * Q * D, fr + K::F_TB, a0, st0);  // rG = B^T w0 (BP1: r)
-      if constexpr (NC == 3) {
-        auto a12 = [&](int m, int k) -> double {
-          const int e = m / (Q * D), u = m - e * (Q * D);
-          return k < Q ? s1[e * P1 + D * Q * LQ + u * LQ + k]
-                       : (k < 2 * Q ? s1[e * P1 + 2 * D * Q * LQ + u * LQ + (k - Q)] : 0.0);
-        };
-        auto st1 = [&](int m, int n, double c0, double c1) {
-          if (n < D) store_r(m, n, 1, c0);
-          if (n + 1 < D) store_r(m, n + 1, 1, c1);
-        };
-        dmma_stage<NW, K::K2Q, K::ND>(ne * Q * D, fr + K::F_GB, a12, st1);  // rB = G^T w1 + B^T w2
-      }
-    }
-    __syncthreads();
-
-    // ---- stage E: rows (e, v=j+Dk), K = a (transposed x) + scatter ---------
-    {
-      auto store = [&](int m, int n, double c0, double c1) {
-        const int e = m / (D * D), v = m - e * (D * D);
-        const int* g = sg + e * D3 + v * D;
-        if (n < D) atomicAdd(y + g[n], c0);
-        if (n + 1 < D) atomicAdd(y + g[n + 1], c1);
-      };
-      if constexpr (NC == 3) {
-        auto aval = [&](int m, int k) -> double {
-          const int e = m / (D * D), v = m - e * (D * D);
-          return k < Q ? s0[e * P0 + v * LQ + k]
-                       : (k < 2 * Q ? s0[e * P0 + D * D * LQ + v * LQ + (k - Q)] : 0.0);
-        };
-        dmma_stage<NW, K::K2Q, K::ND>(ne * D * D, fr + K::F_GB, aval, store);
-      } else {
-        auto aval = [&](int m, int k) -> double {
-          const int e = m / (D * D), v = m - e * (D * D);
-          return k < Q ? s0[e * P0 + v * LQ + k] : 0.0;
-        };
-        dmma_stage<NW, K::KQ, K::ND>(ne * D * D, fr + K::F_TB, aval, store);
-      }
-    }
-    __syncthreads();
   }
-}
+
+  // rows (e, r = a + Q b): z-contraction, D (from smem), transposed z -> W [s][k][a][b]
+  __device__ __forceinline__ static void stage_c(const Tables<D, Q>&, const double* s0,
+                                                 const double* db, double* s1, int ne, double* fr) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, rr = lane >> 2, cc = lane & 3;
+    const int rows = ne * Q * Q;
+    const int src = (lane & ~3) + ((lane & 3) >> 1);
+    for (int m0 = warp * 8; m0 < rows; m0 += NW * 8) {
+      const int m = m0 + rr;
+      const bool ok = m < rows;
+      const int e = ok ? m / (Q * Q) : 0, r = ok ? m - e * (Q * Q) : 0;
+      double g[NC][NQ][2];
+#pragma unroll
+      for (int s = 0; s < NC; ++s)
+#pragma unroll
+        for (int nt = 0; nt < NQ; ++nt) g[s][nt][0] = g[s][nt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KD; ++ks) {
+        const int k = ks * 4 + cc;
+#pragma unroll
+        for (int s = 0; s < NC; ++s) {
+          const double a = (ok && k < D) ? s0[e * P0 + s * Q * Q * LS + r * LS + k] : 0.0;
+          const double* f = fr + ((NC == 3 && s == 2) ? F_CG : F_CB);
+#pragma unroll
+          for (int nt = 0; nt < NQ; ++nt) dmma884(g[s][nt][0], g[s][nt][1], a, f[(nt * KD + ks) * 32 + lane]);
+        }
+      }
+      // pointwise D on the fragments: entry (m, c = 8nt + 2cc + h), qp = r + Q^2 c
+      const double* pe = db + e * G::PS + r;
+#pragma unroll
+      for (int nt = 0; nt < NQ; ++nt) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = nt * 8 + 2 * cc + h;
+          if (ok && c < Q) {
+            const double* pc = pe + c * Q * Q;
+            if constexpr (NC == 3) {
+              const double d00 = pc[0], d01 = pc[Q3], d02 = pc[2 * Q3];
+              const double d11 = pc[3 * Q3], d12 = pc[4 * Q3], d22 = pc[5 * Q3];
+              const double g0 = g[0][nt][h], g1 = g[1][nt][h], g2 = g[2][nt][h];
+              g[0][nt][h] = fma(d02, g2, fma(d01, g1, d00 * g0));
+              g[1][nt][h] = fma(d12, g2, fma(d11, g1, d01 * g0));
+              g[2][nt][h] = fma(d22, g2, fma(d12, g1, d02 * g0));
+            } else {
+              g[0][nt][h] *= pc[0];
+            }
+          } else {
+#pragma unroll
+            for (int s = 0; s < NC; ++s) g[s][nt][h] = 0.0;
+          }
+        }
+      }
+      // transposed z: W_s[m][k'] = sum_c Mat_s[c][k'] o_s[m][c]; A fragments from
+      // C fragments: A(row, 4ks + L%4) lives in lane 4(L/4) + 2(ks%2) + (L%4)/2,
+      // register (L%2), of C tile ks/2.
+      double w[NC][ND][2];
+#pragma unroll
+      for (int s = 0; s < NC; ++s)
+#pragma unroll
+        for (int nt = 0; nt < ND; ++nt) w[s][nt][0] = w[s][nt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KQ; ++ks) {
+        const int tile = ks >> 1, sl = src + 2 * (ks & 1);
+#pragma unroll
+        for (int s = 0; s < NC; ++s) {
+          const double v0 = __shfl_sync(0xffffffffu, g[s][tile][0], sl);
+          const double v1 = __shfl_sync(0xffffffffu, g[s][tile][1], sl);
+          const double a = (lane & 1) ? v1 : v0;
+          const double* f = fr + ((NC == 3 && s == 2) ? F_TG : F_TB);
+#pragma unroll
+          for (int nt = 0; nt < ND; ++nt) dmma884(w[s][nt][0], w[s][nt][1], a, f[(nt * KQ + ks) * 32 + lane]);
+        }
+      }
+      if (ok) {
+        const int a = r % Q, b = r / Q;
+        double* o = s1 + e * P1 + a * LQ + b;
+#pragma unroll
+        for (int nt = 0; nt < ND; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int kk = nt * 8 + 2 * cc + h;
+            if (kk < D) {
+#pragma unroll
+              for (int s = 0; s < NC; ++s) o[s * D * Q * LQ + kk * Q * LQ] = w[s][nt][h];
+            }
+          }
+      }
+    }
+  }
+
+  // rows (e, u = a + Q k), K = b (transposed y) -> R [s][k][j][a]
+  __device__ __forceinline__ static void stage_d(const Tables<D, Q>&, const double* s1, double* s0,
+                                                 int ne, double* fr) {
+    auto store_r = [&](int m, int j, int s, double v) {
+      const int e = m / (Q * D), u = m - e * (Q * D);
+      s0[e * P0 + s * D * D * LQ + ((u / Q) * D + j) * LQ + (u % Q)] = v;
+    };
+    auto a0 = [&](int m, int k) -> double {
+      const int e = m / (Q * D), u = m - e * (Q * D);
+      return k < Q ? s1[e * P1 + u * LQ + k] : 0.0;
+    };
+    auto st0 = [&](int m, int n, double c0, double c1) {
+      if (n < D) store_r(m, n, 0, c0);
+      if (n + 1 < D) store_r(m, n + 1, 0, c1);
+    };
+    dmma_stage<NW, KQ, ND>(ne * Q * D, fr + F_TB, a0, st0);  // rG = B^T w0 (BP1: r = B^T w)
+    if constexpr (NC == 3) {
+      auto a12 = [&](int m, int k) -> double {
+        const int e = m / (Q * D), u = m - e * (Q * D);
+        return k < Q ? s1[e * P1 + D * Q * LQ + u * LQ + k]
+                     : (k < 2 * Q ? s1[e * P1 + 2 * D * Q * LQ + u * LQ + (k - Q)] : 0.0);
+      };
+      auto st1 = [&](int m, int n, double c0, double c1) {
+        if (n < D) store_r(m, n, 1, c0);
+        if (n + 1 < D) store_r(m, n + 1, 1, c1);
+      };
+      dmma_stage<NW, K2Q, ND>(ne * Q * D, fr + F_GB, a12, st1);  // rB = G^T w1 + B^T w2
+    }
+  }
+
+  // rows (e, v = j + D k), K = a (transposed x) -> atomic scatter-add
+  __device__ __forceinline__ static void stage_e(const Tables<D, Q>&, const double* s0,
+                                                 const int* gslot, double* y, int ne, double* fr) {
+    auto store = [&](int m, int n, double c0, double c1) {
+      const int e = m / (D * D), v = m - e * (D * D);
+      const int* g = gslot + e * G::GS + v * D;
+      if (n < D) atomicAdd(y + g[n], c0);
+      if (n + 1 < D) atomicAdd(y + g[n + 1], c1);
+    };
+    if constexpr (NC == 3) {
+      auto aval = [&](int m, int k) -> double {
+        const int e = m / (D * D), v = m - e * (D * D);
+        return k < Q ? s0[e * P0 + v * LQ + k]
+                     : (k < 2 * Q ? s0[e * P0 + D * D * LQ + v * LQ + (k - Q)] : 0.0);
+      };
+      dmma_stage<NW, K2Q, ND>(ne * D * D, fr + F_GB, aval, store);
+    } else {
+      auto aval = [&](int m, int k) -> double {
+        const int e = m / (D * D), v = m - e * (D * D);
+        return k < Q ? s0[e * P0 + v * LQ + k] : 0.0;
+      };
+      dmma_stage<NW, KQ, ND>(ne * D * D, fr + F_TB, aval, store);
+    }
+  }
+};
 
 }  // namespace fk

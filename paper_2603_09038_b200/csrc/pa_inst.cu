@@ -1,14 +1,17 @@
 // pa_inst.cu — explicit instantiation of the fused kernels for ONE order.
 // Compiled once per order with -DFK_P=<p> (the build runs the eight
 // compilations in parallel); each object exports fk_register_p<p>().
+//
+// Several launch geometries (elements per CTA E, threads T) are compiled per
+// (kind, p, q, variant); the first registered is the default, the others are
+// selectable (FK_CFG=<index>) for the tuning sweep recorded in DESIGN.md.
 #include <cstring>
 
 #include "fk_internal.h"
 #include "pa_diag.cuh"
 #include "pa_dfma.cuh"
-#if FK_HAVE_DMMA
 #include "pa_dmma.cuh"
-#endif
+#include "pa_pipe.cuh"
 
 #ifndef FK_P
 #error "compile with -DFK_P=<order>"
@@ -17,19 +20,18 @@
 namespace fk {
 namespace {
 
-// Launch geometry: E elements per CTA so that E*q^2 lines (stage C, the
-// heaviest) fill whole warps, T = E*q^2 rounded up to a warp multiple.
-constexpr int pick_E(int Q) { return (288 / (Q * Q)) > 0 ? (288 / (Q * Q)) : 1; }
-constexpr int pick_T(int Q) { return ((pick_E(Q) * Q * Q + 31) / 32) * 32; }
+constexpr int round32(int n) { return ((n + 31) / 32) * 32; }
+// stage C (q^2 lines per element) is the heaviest: E*q^2 lines ~ 288
+constexpr int base_E(int Q) { return (288 / (Q * Q)) > 0 ? (288 / (Q * Q)) : 1; }
 
-template <int D, int Q, int NC>
-void launch_dfma(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
-  constexpr int E = pick_E(Q), T = pick_T(Q);
+template <int D, int Q, int NC, class Body>
+void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
   Tables<D, Q> tb;
   std::memcpy(tb.B, v.B, sizeof(tb.B));
   std::memcpy(tb.G, v.G, sizeof(tb.G));
-  pa_dfma_kernel<D, Q, NC, E, T><<<blocks, T, LineLayout<D, Q, NC>::smem_bytes(E), s>>>(
-      tb, x, y, v.gids, v.pa, v.mask, v.nel);
+  pa_pipe_kernel<D, Q, NC, Body>
+      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body::E, Body::EXTRA>::BYTES, s>>>(
+          tb, x, y, v.gids, v.pa, v.ebits, v.nel);
 }
 
 template <int D, int Q, int NC>
@@ -40,50 +42,34 @@ void launch_diag(const OpView& v, double* diag, int64_t nel, int blocks, cudaStr
   diagonal_kernel<D, Q, NC><<<blocks, 128, 0, s>>>(tb, diag, v.gids, v.pa, nel);
 }
 
-template <int D, int Q, int NC>
-KernelEntry entry_dfma() {
-  constexpr int E = pick_E(Q), T = pick_T(Q);
+template <int D, int Q, int NC, class Body>
+KernelEntry entry(int variant, int cfg) {
   KernelEntry k;
   k.nc = NC;
   k.d = D;
   k.q = Q;
-  k.variant = FK_VARIANT_DFMA;
-  k.E = E;
-  k.T = T;
-  k.smem = LineLayout<D, Q, NC>::smem_bytes(E);
-  k.func = reinterpret_cast<const void*>(&pa_dfma_kernel<D, Q, NC, E, T>);
-  k.launch = &launch_dfma<D, Q, NC>;
+  k.variant = variant;
+  k.cfg = cfg;
+  k.E = Body::E;
+  k.T = Body::T;
+  k.smem = PipeSmem<D, Q, NC, Body::E, Body::EXTRA>::BYTES;
+  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body>);
+  k.launch = &launch_pipe<D, Q, NC, Body>;
   k.diag = &launch_diag<D, Q, NC>;
   return k;
 }
 
-#if FK_HAVE_DMMA
 template <int D, int Q, int NC>
-void launch_dmma(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
-  using K = DmmaConfig<D, Q, NC>;
-  Tables<D, Q> tb;
-  std::memcpy(tb.B, v.B, sizeof(tb.B));
-  std::memcpy(tb.G, v.G, sizeof(tb.G));
-  pa_dmma_kernel<D, Q, NC><<<blocks, K::T, K::smem_bytes(), s>>>(tb, x, y, v.gids, v.pa, v.mask,
-                                                                  v.nel);
+void add_all(std::vector<KernelEntry>& out) {
+  constexpr int E0 = base_E(Q);
+  constexpr int E1 = E0 / 2 > 0 ? E0 / 2 : 1;
+  constexpr int E2 = E0 / 4 > 0 ? E0 / 4 : 1;
+  out.push_back(entry<D, Q, NC, DfmaBody<D, Q, NC, E1, round32(E1 * Q * Q)>>(FK_VARIANT_DFMA, 0));
+  out.push_back(entry<D, Q, NC, DfmaBody<D, Q, NC, E0, round32(E0 * Q * Q)>>(FK_VARIANT_DFMA, 1));
+  out.push_back(entry<D, Q, NC, DfmaBody<D, Q, NC, E2, round32(E2 * Q * Q)>>(FK_VARIANT_DFMA, 2));
+  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>>(FK_VARIANT_DMMA, 0));
+  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E0, 256>>(FK_VARIANT_DMMA, 1));
 }
-
-template <int D, int Q, int NC>
-KernelEntry entry_dmma() {
-  using K = DmmaConfig<D, Q, NC>;
-  KernelEntry k;
-  k.nc = NC;
-  k.d = D;
-  k.q = Q;
-  k.variant = FK_VARIANT_DMMA;
-  k.E = K::E;
-  k.T = K::T;
-  k.smem = K::smem_bytes();
-  k.func = reinterpret_cast<const void*>(&pa_dmma_kernel<D, Q, NC>);
-  k.launch = &launch_dmma<D, Q, NC>;
-  return k;
-}
-#endif
 
 }  // namespace
 }  // namespace fk
@@ -91,14 +77,10 @@ KernelEntry entry_dmma() {
 #define FK_CAT2(a, b) a##b
 #define FK_CAT(a, b) FK_CAT2(a, b)
 
-extern "C++" void FK_CAT(fk_register_p, FK_P)(std::vector<fk::KernelEntry>& out) {
+void FK_CAT(fk_register_p, FK_P)(std::vector<fk::KernelEntry>& out) {
   constexpr int D = FK_P + 1;
-  out.push_back(fk::entry_dfma<D, FK_P + 2, 3>());
-  out.push_back(fk::entry_dfma<D, FK_P + 1, 3>());
-  out.push_back(fk::entry_dfma<D, FK_P + 2, 1>());
-  out.push_back(fk::entry_dfma<D, FK_P + 1, 1>());
-#if FK_HAVE_DMMA
-  out.push_back(fk::entry_dmma<D, FK_P + 2, 3>());
-  out.push_back(fk::entry_dmma<D, FK_P + 2, 1>());
-#endif
+  fk::add_all<D, FK_P + 2, 3>(out);
+  fk::add_all<D, FK_P + 2, 1>(out);
+  fk::add_all<D, FK_P + 1, 3>(out);
+  fk::add_all<D, FK_P + 1, 1>(out);
 }

@@ -219,6 +219,19 @@ class PAOperator:
         _lib.check(self._lib.fk_op_set_variant(self._h, _lib.VARIANTS[variant]))
         self.info = self._info()
 
+    def set_config(self, variant: str, cfg: int) -> None:
+        """Pick compiled launch geometry ``cfg`` of ``variant`` ("dfma"/"dmma")."""
+        if variant not in ("dfma", "dmma"):
+            raise ValueError(f"variant must be 'dfma' or 'dmma', got {variant!r}")
+        _lib.check(self._lib.fk_op_set_config(self._h, _lib.VARIANTS[variant], int(cfg)))
+        self.info = self._info()
+
+    @property
+    def launch(self) -> tuple[int, int, int]:
+        """(elements per CTA, threads per CTA, persistent CTAs)."""
+        i = self._info()
+        return i.elems_per_block, i.threads_per_block, i.blocks
+
     # -- vectors --------------------------------------------------------------
 
     def zeros(self):

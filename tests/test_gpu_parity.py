@@ -117,6 +117,29 @@ def test_apply_matches_oracle_all_orders(variant, kind, p, qoff):
     assert normwise(y, P.apply(x)) <= PARITY_TOL
 
 
+LAUNCH_CONFIGS = [("dfma", 0), ("dfma", 1), ("dfma", 2), ("dmma", 0), ("dmma", 1)]
+
+
+@pytest.mark.parametrize("variant,cfg", LAUNCH_CONFIGS)
+@pytest.mark.parametrize("kind", ["mass", "diffusion"])
+@pytest.mark.parametrize("p", range(1, 9))
+def test_every_launch_config(variant, cfg, kind, p):
+    """Every compiled (variant, E, T) geometry, incl. the Dirichlet-bit path and
+    meshes whose element count does not fill the last batch."""
+    n = (5, 3, 3) if p <= 4 else (3, 2, 3)
+    P = bp.Problem(kind, *n, p)
+    x = np.random.default_rng(p).standard_normal(P.ndof)
+    for dirichlet in (False, True):
+        op = make(kind, n, p, dirichlet=dirichlet)
+        try:
+            op.set_config(variant, cfg)
+        except NotImplementedError as ex:  # geometry exceeds 227 KB smem at this order
+            pytest.skip(str(ex))
+        y = op.apply(dev(x)).cpu().numpy()
+        ref = P.constrained_apply(x, P.boundary()) if dirichlet else P.apply(x)
+        assert normwise(y, ref) <= PARITY_TOL, (op.launch, dirichlet)
+
+
 @pytest.mark.parametrize("n", [(1, 1, 1), (3, 1, 2), (1, 5, 1), (7, 3, 5)])
 @pytest.mark.parametrize("p", [1, 4, 7])
 def test_ragged_meshes(n, p):
