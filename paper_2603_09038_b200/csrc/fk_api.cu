@@ -130,7 +130,9 @@ int select_kernel(fk_op* op, int variant) {
     FK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->func, k->T, k->smem));
     if (occ < 1) return fail(FK_EUNSUPPORTED, "fused kernel does not fit on an SM (smem %zu)", k->smem);
     const int64_t nbatch = (op->nel + k->E - 1) / k->E;
-    op->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ * op->num_sms));
+    op->blocks = k->persist
+                     ? (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ * op->num_sms))
+                     : (int)std::max<int64_t>(1, nbatch);
   }
   return FK_OK;
 }

@@ -18,6 +18,7 @@ using DiagFn = void (*)(const OpView&, double* diag, int64_t nel, int blocks, cu
 struct KernelEntry {
   int nc = 0, d = 0, q = 0, variant = 0, cfg = 0;
   int E = 0, T = 0;
+  bool persist = true;  // persistent grid (batches strided over CTAs) or one batch per CTA
   size_t smem = 0;
   const void* func = nullptr;
   LaunchFn launch = nullptr;

@@ -11,23 +11,46 @@
 //
 // MFEM-style stage sharing: BP3 costs 2(4qd^3+6q^2d^2+6q^3d)+15q^3 flops per
 // element instead of the reference's three independent chains
-// (apply_gradient_3d, tensor.py:244-260).  Each thread keeps its line in
-// registers; one 8-byte shared load of the line feeds q (or 2q, 3q) FMAs.
+// (apply_gradient_3d, tensor.py:244-260).  Each thread keeps NL lines in
+// registers; one 8-byte shared load of a line value feeds q (2q, 3q) FMAs and
+// one basis-table load feeds NL lines.
 //
-// Basis tables: sm_100a ptxas turns every double kernel-parameter operand
-// into LDCU + uniform-register traffic and, when it hoists the 2qd table
-// entries out of the persistent loop, spills the uniform register file
-// (measured: ~1000 of 2000 warp instructions per element were R2UR / IMAD /
-// LDCU moves).  The tables therefore live in shared memory as 16-byte-aligned
-// rows (B[a][*], G[a][*] and the transposes) and each row is read with
-// LDS.128 broadcasts right where it is used (__syncthreads between stages
-// keeps the compiler from hoisting them): 0.5 load per table entry, no
-// register pressure from the tables.
+// Basis tables (measured): sm_100a ptxas feeds double
+// constants to DFMA through uniform registers (LDCU + UR operand).  With the
+// 2qd table entries loop-invariant it hoists them out of the persistent loop,
+// overflows the 63-entry uniform register file and spills through vector
+// registers (R2UR / MOV.SPILL: ~1000 of 2000 warp instructions per element);
+// reading rows from shared memory instead costs LDS wavefronts the kernel
+// does not have.  The kernel parameter therefore carries TWO copies of the
+// tables and batch `it` reads copy it&1: the loads stay loop-variant, so each
+// row is fetched (LDCU.128, 2 entries) right where it is used and shared by
+// the NL lines of the thread.
 #pragma once
 
 #include "pa_common.cuh"
 
 namespace fk {
+
+template <int D, int Q>
+struct __align__(16) RowTables {
+  static constexpr int DP = D + (D & 1), QP = Q + (Q & 1);  // 16-byte row pitch
+  static constexpr int TB = 0, TG = Q * DP, TBT = 2 * Q * DP, TGT = 2 * Q * DP + D * QP;
+  static constexpr int SZ = 2 * Q * DP + 2 * D * QP;
+  double t[2][SZ];  // two copies of: B[a][i], G[a][i] rows; Bt[i][a], Gt[i][a] rows
+};
+
+// Run f(t0) over the stage's lines t0 = threadIdx.x + k*STEP < n.  When every
+// line fits in one pass (LMAX <= STEP, the configured geometries) there is no
+// loop at all, so nothing invites ptxas to hoist basis-table loads into
+// vector registers (and shuttle them back with R2UR for every DFMA).
+template <int STEP, int LMAX, typename F>
+__device__ __forceinline__ void lines_loop(int n, F f) {
+  if constexpr (LMAX <= STEP) {
+    if ((int)threadIdx.x < n) f((int)threadIdx.x);
+  } else {
+    for (int t0 = threadIdx.x; t0 < n; t0 += STEP) f(t0);
+  }
+}
 
 template <int N>
 __device__ __forceinline__ void ld_row(const double* __restrict__ p, double (&r)[N]) {
@@ -40,274 +63,323 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, double (&r)
   if constexpr (N & 1) r[N - 1] = p[N - 1];
 }
 
-template <int D, int Q, int NC, int E_, int T_>
+template <int D, int Q, int NC, int E_, int T_, int NL_>
 struct DfmaBody {
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
+  using Tab = RowTables<D, Q>;
   static constexpr int LS = L::LS, LQ = L::LQ, P0 = L::P0, P1 = L::P1, Q3 = L::Q3;
   static constexpr int XS = D * D * LS;
-  static constexpr int DP = D + (D & 1), QP = Q + (Q & 1);  // 16-byte row pitch
-  // smem table offsets (doubles): B[a][i], G[a][i] rows of D; Bt[i][a], Gt[i][a] rows of Q
-  static constexpr int TB = 0, TG = TB + Q * DP, TBT = TG + Q * DP, TGT = TBT + D * QP;
-  static constexpr int E = E_, T = T_, EXTRA = TGT + D * QP;
+  static constexpr int DP = Tab::DP, QP = Tab::QP;
+  static constexpr int E = E_, T = T_, EXTRA = 0;
+  static constexpr int NL = NL_;                                        // lines per thread
+  static constexpr int NLC = (NC == 3 && 6 * D * NL_ > 60) ? 1 : NL_;  // stage C (register-heavy)
 
-  __device__ static void init(const Tables<D, Q>& tb, double* t) {
-    for (int n = threadIdx.x; n < Q * D; n += T) {
-      const int a = n / D, i = n % D;
-      t[TB + a * DP + i] = tb.B[n];
-      t[TG + a * DP + i] = tb.G[n];
-      t[TBT + i * QP + a] = tb.B[n];
-      t[TGT + i * QP + a] = tb.G[n];
-    }
+  static void fill(Tab& tb, const double* B, const double* Gr) {
+    for (int c = 0; c < 2; ++c)
+      for (int a = 0; a < Q; ++a)
+        for (int i = 0; i < D; ++i) {
+          tb.t[c][Tab::TB + a * DP + i] = B[a * D + i];
+          tb.t[c][Tab::TG + a * DP + i] = Gr[a * D + i];
+          tb.t[c][Tab::TBT + i * QP + a] = B[a * D + i];
+          tb.t[c][Tab::TGT + i * QP + a] = Gr[a * D + i];
+        }
   }
 
+  __device__ static void init(const Tab&, double*) {}
+
   // X [v=(j,k)][i] -> T1 [s][a][k][j]
-  __device__ __forceinline__ static void stage_a(const Tables<D, Q>&, const double* xb, double* s1,
-                                                 int ne, const double* tab) {
-    for (int t = threadIdx.x; t < ne * D * D; t += T) {
-      const int e = t / (D * D), v = t - e * (D * D);
-      const double* in = xb + e * XS + v * LS;
-      double xr[D];
+  __device__ __forceinline__ static void stage_a(const Tab& tb, int it, const double* xb,
+                                                 double* s1, int ne, double*) {
+    const double* tab = tb.t[it & 1];
+    const int n = ne * D * D;
+    lines_loop<NL * T, E * D * D>(n, [&](int t0) {
+      double xr[NL][D];
+      double* o[NL];
+      bool ok[NL];
 #pragma unroll
-      for (int i = 0; i < D; ++i) xr[i] = in[i];
-      double* o = s1 + e * P1 + (v / D) * LS + (v % D);
+      for (int h = 0; h < NL; ++h) {
+        const int t = t0 + h * T;
+        ok[h] = t < n;
+        const int tt = ok[h] ? t : t0;
+        const int e = tt / (D * D), v = tt - e * (D * D);
+        const double* in = xb + e * XS + v * LS;
+#pragma unroll
+        for (int i = 0; i < D; ++i) xr[h][i] = in[i];
+        o[h] = s1 + e * P1 + (v / D) * LS + (v % D);
+      }
 #pragma unroll
       for (int a = 0; a < Q; ++a) {
         double br[D];
-        ld_row(tab + TB + a * DP, br);
-        double bx = br[0] * xr[0];
+        ld_row(tab + Tab::TB + a * DP, br);
 #pragma unroll
-        for (int i = 1; i < D; ++i) bx = fma(br[i], xr[i], bx);
-        o[a * D * LS] = bx;
+        for (int h = 0; h < NL; ++h) {
+          double bx = br[0] * xr[h][0];
+#pragma unroll
+          for (int i = 1; i < D; ++i) bx = fma(br[i], xr[h][i], bx);
+          if (ok[h]) o[h][a * D * LS] = bx;
+        }
         if constexpr (NC == 3) {
           double gr[D];
-          ld_row(tab + TG + a * DP, gr);
-          double gx = gr[0] * xr[0];
+          ld_row(tab + Tab::TG + a * DP, gr);
 #pragma unroll
-          for (int i = 1; i < D; ++i) gx = fma(gr[i], xr[i], gx);
-          o[Q * D * LS + a * D * LS] = gx;
+          for (int h = 0; h < NL; ++h) {
+            double gx = gr[0] * xr[h][0];
+#pragma unroll
+            for (int i = 1; i < D; ++i) gx = fma(gr[i], xr[h][i], gx);
+            if (ok[h]) o[h][Q * D * LS + a * D * LS] = gx;
+          }
         }
       }
-    }
+    });
   }
 
   // T1 [s][a][k][j] (line u = k + D a) -> T2 [s][b][a][k]
-  __device__ __forceinline__ static void stage_b(const Tables<D, Q>&, const double* s1, double* s0,
-                                                 int ne, const double* tab) {
-    for (int t = threadIdx.x; t < ne * D * Q; t += T) {
-      const int e = t / (D * Q), u = t - e * (D * Q);
-      const double* in = s1 + e * P1 + u * LS;
-      double bx[D];
+  __device__ __forceinline__ static void stage_b(const Tab& tb, int it, const double* s1, double* s0,
+                                                 int ne, double*) {
+    const double* tab = tb.t[it & 1];
+    const int n = ne * D * Q;
+    lines_loop<NL * T, E * D * Q>(n, [&](int t0) {
+      double bx[NL][D], gx[NL][D];
+      double* o[NL];
+      bool ok[NL];
 #pragma unroll
-      for (int j = 0; j < D; ++j) bx[j] = in[j];
-      const int k = u % D, a = u / D;
-      double* o = s0 + e * P0 + a * LS + k;
-      if constexpr (NC == 3) {
-        double gx[D];
+      for (int h = 0; h < NL; ++h) {
+        const int t = t0 + h * T;
+        ok[h] = t < n;
+        const int tt = ok[h] ? t : t0;
+        const int e = tt / (D * Q), u = tt - e * (D * Q);
+        const double* in = s1 + e * P1 + u * LS;
 #pragma unroll
-        for (int j = 0; j < D; ++j) gx[j] = in[Q * D * LS + j];
-#pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          double br[D], gr[D];
-          ld_row(tab + TB + b * DP, br);
-          ld_row(tab + TG + b * DP, gr);
-          double c0 = br[0] * gx[0];
-          double c1 = gr[0] * bx[0];
-          double c2 = br[0] * bx[0];
-#pragma unroll
-          for (int j = 1; j < D; ++j) {
-            c0 = fma(br[j], gx[j], c0);
-            c1 = fma(gr[j], bx[j], c1);
-            c2 = fma(br[j], bx[j], c2);
-          }
-          o[b * Q * LS] = c0;
-          o[Q * Q * LS + b * Q * LS] = c1;
-          o[2 * Q * Q * LS + b * Q * LS] = c2;
+        for (int j = 0; j < D; ++j) {
+          bx[h][j] = in[j];
+          if constexpr (NC == 3) gx[h][j] = in[Q * D * LS + j];
         }
-      } else {
+        o[h] = s0 + e * P0 + (u / D) * LS + (u % D);
+      }
 #pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          double br[D];
-          ld_row(tab + TB + b * DP, br);
-          double c = br[0] * bx[0];
+      for (int b = 0; b < Q; ++b) {
+        double br[D];
+        ld_row(tab + Tab::TB + b * DP, br);
+        if constexpr (NC == 3) {
+          double gr[D];
+          ld_row(tab + Tab::TG + b * DP, gr);
 #pragma unroll
-          for (int j = 1; j < D; ++j) c = fma(br[j], bx[j], c);
-          o[b * Q * LS] = c;
+          for (int h = 0; h < NL; ++h) {
+            double c0 = br[0] * gx[h][0];
+            double c1 = gr[0] * bx[h][0];
+            double c2 = br[0] * bx[h][0];
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+              c0 = fma(br[j], gx[h][j], c0);
+              c1 = fma(gr[j], bx[h][j], c1);
+              c2 = fma(br[j], bx[h][j], c2);
+            }
+            if (ok[h]) {
+              o[h][b * Q * LS] = c0;
+              o[h][Q * Q * LS + b * Q * LS] = c1;
+              o[h][2 * Q * Q * LS + b * Q * LS] = c2;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < NL; ++h) {
+            double c = br[0] * bx[h][0];
+#pragma unroll
+            for (int j = 1; j < D; ++j) c = fma(br[j], bx[h][j], c);
+            if (ok[h]) o[h][b * Q * LS] = c;
+          }
         }
       }
-    }
+    });
   }
 
   // T2 [s][b][a][k] (line r = a + Q b) + D -> W [s][k][a][b]
-  __device__ __forceinline__ static void stage_c(const Tables<D, Q>&, const double* s0,
-                                                 const double* db, double* s1, int ne,
-                                                 const double* tab) {
-    for (int t = threadIdx.x; t < ne * Q * Q; t += T) {
-      const int e = t / (Q * Q), r = t - e * (Q * Q);
-      const double* in = s0 + e * P0 + r * LS;
-      const double* pe = db + e * G::PS + r;
-      const int a = r % Q, b = r / Q;
-      double* o = s1 + e * P1 + a * LQ + b;
-      if constexpr (NC == 3) {
-        double t0[D], t1[D], t2[D], w0[D], w1[D], w2[D];
+  __device__ __forceinline__ static void stage_c(const Tab& tb, int it, const double* s0,
+                                                 const double* db, double* s1, int ne, double*) {
+    const double* tab = tb.t[it & 1];
+    const int n = ne * Q * Q;
+    constexpr int NS = NC;
+    lines_loop<NLC * T, E * Q * Q>(n, [&](int t0) {
+      double tin[NLC][NS][D], w[NLC][NS][D];
+      const double* pe[NLC];
+      double* o[NLC];
+      bool ok[NLC];
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-          t0[k] = in[k];
-          t1[k] = in[Q * Q * LS + k];
-          t2[k] = in[2 * Q * Q * LS + k];
-          w0[k] = 0.0;
-          w1[k] = 0.0;
-          w2[k] = 0.0;
-        }
+      for (int h = 0; h < NLC; ++h) {
+        const int t = t0 + h * T;
+        ok[h] = t < n;
+        const int tt = ok[h] ? t : t0;
+        const int e = tt / (Q * Q), r = tt - e * (Q * Q);
+        const double* in = s0 + e * P0 + r * LS;
 #pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double br[D], gr[D];
-          ld_row(tab + TB + c * DP, br);
-          ld_row(tab + TG + c * DP, gr);
-          double g0 = br[0] * t0[0];
-          double g1 = br[0] * t1[0];
-          double g2 = gr[0] * t2[0];
-#pragma unroll
-          for (int k = 1; k < D; ++k) {
-            g0 = fma(br[k], t0[k], g0);
-            g1 = fma(br[k], t1[k], g1);
-            g2 = fma(gr[k], t2[k], g2);
-          }
-          const double* pc = pe + c * Q * Q;
-          const double d00 = pc[0 * Q3], d01 = pc[1 * Q3], d02 = pc[2 * Q3];
-          const double d11 = pc[3 * Q3], d12 = pc[4 * Q3], d22 = pc[5 * Q3];
-          const double o0 = fma(d02, g2, fma(d01, g1, d00 * g0));
-          const double o1 = fma(d12, g2, fma(d11, g1, d01 * g0));
-          const double o2 = fma(d22, g2, fma(d12, g1, d02 * g0));
+        for (int s = 0; s < NS; ++s)
 #pragma unroll
           for (int k = 0; k < D; ++k) {
-            w0[k] = fma(br[k], o0, w0[k]);
-            w1[k] = fma(br[k], o1, w1[k]);
-            w2[k] = fma(gr[k], o2, w2[k]);
+            tin[h][s][k] = in[s * Q * Q * LS + k];
+            w[h][s][k] = 0.0;
+          }
+        pe[h] = db + e * G::PS + r;
+        o[h] = s1 + e * P1 + (r % Q) * LQ + (r / Q);
+      }
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        double br[D], gr[D];
+        ld_row(tab + Tab::TB + c * DP, br);
+        if constexpr (NC == 3) ld_row(tab + Tab::TG + c * DP, gr);
+#pragma unroll
+        for (int h = 0; h < NLC; ++h) {
+          const double* pc = pe[h] + c * Q * Q;
+          if constexpr (NC == 3) {
+            double g0 = br[0] * tin[h][0][0];
+            double g1 = br[0] * tin[h][1][0];
+            double g2 = gr[0] * tin[h][2][0];
+#pragma unroll
+            for (int k = 1; k < D; ++k) {
+              g0 = fma(br[k], tin[h][0][k], g0);
+              g1 = fma(br[k], tin[h][1][k], g1);
+              g2 = fma(gr[k], tin[h][2][k], g2);
+            }
+            const double d00 = pc[0 * Q3], d01 = pc[1 * Q3], d02 = pc[2 * Q3];
+            const double d11 = pc[3 * Q3], d12 = pc[4 * Q3], d22 = pc[5 * Q3];
+            const double o0 = fma(d02, g2, fma(d01, g1, d00 * g0));
+            const double o1 = fma(d12, g2, fma(d11, g1, d01 * g0));
+            const double o2 = fma(d22, g2, fma(d12, g1, d02 * g0));
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              w[h][0][k] = fma(br[k], o0, w[h][0][k]);
+              w[h][1][k] = fma(br[k], o1, w[h][1][k]);
+              w[h][2][k] = fma(gr[k], o2, w[h][2][k]);
+            }
+          } else {
+            double g = br[0] * tin[h][0][0];
+#pragma unroll
+            for (int k = 1; k < D; ++k) g = fma(br[k], tin[h][0][k], g);
+            const double oo = pc[0] * g;
+#pragma unroll
+            for (int k = 0; k < D; ++k) w[h][0][k] = fma(br[k], oo, w[h][0][k]);
           }
         }
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          o[k * Q * LQ] = w0[k];
-          o[D * Q * LQ + k * Q * LQ] = w1[k];
-          o[2 * D * Q * LQ + k * Q * LQ] = w2[k];
-        }
-      } else {
-        double tt[D], w[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          tt[k] = in[k];
-          w[k] = 0.0;
-        }
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double br[D];
-          ld_row(tab + TB + c * DP, br);
-          double g = br[0] * tt[0];
-#pragma unroll
-          for (int k = 1; k < D; ++k) g = fma(br[k], tt[k], g);
-          const double oo = pe[c * Q * Q] * g;
-#pragma unroll
-          for (int k = 0; k < D; ++k) w[k] = fma(br[k], oo, w[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < D; ++k) o[k * Q * LQ] = w[k];
       }
-    }
+#pragma unroll
+      for (int h = 0; h < NLC; ++h) {
+        if (!ok[h]) continue;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+          for (int k = 0; k < D; ++k) o[h][s * D * Q * LQ + k * Q * LQ] = w[h][s][k];
+      }
+    });
   }
 
   // W [s][k][a][b] (line u = a + Q k) -> R [s][k][j][a]
-  __device__ __forceinline__ static void stage_d(const Tables<D, Q>&, const double* s1, double* s0,
-                                                 int ne, const double* tab) {
-    for (int t = threadIdx.x; t < ne * Q * D; t += T) {
-      const int e = t / (Q * D), u = t - e * (Q * D);
-      const double* in = s1 + e * P1 + u * LQ;
-      const int a = u % Q, k = u / Q;
-      double* o = s0 + e * P0 + k * D * LQ + a;
-      if constexpr (NC == 3) {
-        double w0[Q], w1[Q], w2[Q];
+  __device__ __forceinline__ static void stage_d(const Tab& tb, int it, const double* s1, double* s0,
+                                                 int ne, double*) {
+    const double* tab = tb.t[it & 1];
+    const int n = ne * Q * D;
+    lines_loop<NL * T, E * Q * D>(n, [&](int t0) {
+      double w[NL][NC][Q];
+      double* o[NL];
+      bool ok[NL];
 #pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          w0[b] = in[b];
-          w1[b] = in[D * Q * LQ + b];
-          w2[b] = in[2 * D * Q * LQ + b];
-        }
+      for (int h = 0; h < NL; ++h) {
+        const int t = t0 + h * T;
+        ok[h] = t < n;
+        const int tt = ok[h] ? t : t0;
+        const int e = tt / (Q * D), u = tt - e * (Q * D);
+        const double* in = s1 + e * P1 + u * LQ;
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-          double bt[Q], gt[Q];
-          ld_row(tab + TBT + j * QP, bt);
-          ld_row(tab + TGT + j * QP, gt);
-          double rg = bt[0] * w0[0];
-          double rb = gt[0] * w1[0];
+        for (int s = 0; s < NC; ++s)
 #pragma unroll
-          for (int b = 1; b < Q; ++b) {
-            rg = fma(bt[b], w0[b], rg);
-            rb = fma(gt[b], w1[b], rb);
+          for (int b = 0; b < Q; ++b) w[h][s][b] = in[s * D * Q * LQ + b];
+        o[h] = s0 + e * P0 + (u / Q) * D * LQ + (u % Q);
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double bt[Q];
+        ld_row(tab + Tab::TBT + j * QP, bt);
+        if constexpr (NC == 3) {
+          double gt[Q];
+          ld_row(tab + Tab::TGT + j * QP, gt);
+#pragma unroll
+          for (int h = 0; h < NL; ++h) {
+            double rg = bt[0] * w[h][0][0];
+            double rb = gt[0] * w[h][1][0];
+#pragma unroll
+            for (int b = 1; b < Q; ++b) {
+              rg = fma(bt[b], w[h][0][b], rg);
+              rb = fma(gt[b], w[h][1][b], rb);
+            }
+#pragma unroll
+            for (int b = 0; b < Q; ++b) rb = fma(bt[b], w[h][2][b], rb);
+            if (ok[h]) {
+              o[h][j * LQ] = rg;
+              o[h][D * D * LQ + j * LQ] = rb;
+            }
           }
+        } else {
 #pragma unroll
-          for (int b = 0; b < Q; ++b) rb = fma(bt[b], w2[b], rb);
-          o[j * LQ] = rg;
-          o[D * D * LQ + j * LQ] = rb;
-        }
-      } else {
-        double w[Q];
+          for (int h = 0; h < NL; ++h) {
+            double rr = bt[0] * w[h][0][0];
 #pragma unroll
-        for (int b = 0; b < Q; ++b) w[b] = in[b];
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          double bt[Q];
-          ld_row(tab + TBT + j * QP, bt);
-          double rr = bt[0] * w[0];
-#pragma unroll
-          for (int b = 1; b < Q; ++b) rr = fma(bt[b], w[b], rr);
-          o[j * LQ] = rr;
+            for (int b = 1; b < Q; ++b) rr = fma(bt[b], w[h][0][b], rr);
+            if (ok[h]) o[h][j * LQ] = rr;
+          }
         }
       }
-    }
+    });
   }
 
   // R [s][k][j][a] (line v = j + D k) -> y (atomic scatter-add)
-  __device__ __forceinline__ static void stage_e(const Tables<D, Q>&, const double* s0,
-                                                 const int* gslot, double* y, int ne,
-                                                 const double* tab) {
-    for (int t = threadIdx.x; t < ne * D * D; t += T) {
-      const int e = t / (D * D), v = t - e * (D * D);
-      const double* in = s0 + e * P0 + v * LQ;
-      const int* g = gslot + e * G::GS + v * D;
-      if constexpr (NC == 3) {
-        double rg[Q], rb[Q];
+  __device__ __forceinline__ static void stage_e(const Tab& tb, int it, const double* s0,
+                                                 const int* gslot, double* y, int ne, double*) {
+    const double* tab = tb.t[it & 1];
+    constexpr int NR = (NC == 3) ? 2 : 1;
+    const int n = ne * D * D;
+    lines_loop<NL * T, E * D * D>(n, [&](int t0) {
+      double rv[NL][NR][Q];
+      const int* g[NL];
+      bool ok[NL];
 #pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          rg[a] = in[a];
-          rb[a] = in[D * D * LQ + a];
-        }
+      for (int h = 0; h < NL; ++h) {
+        const int t = t0 + h * T;
+        ok[h] = t < n;
+        const int tt = ok[h] ? t : t0;
+        const int e = tt / (D * D), v = tt - e * (D * D);
+        const double* in = s0 + e * P0 + v * LQ;
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-          double bt[Q], gt[Q];
-          ld_row(tab + TBT + i * QP, bt);
-          ld_row(tab + TGT + i * QP, gt);
-          double acc = gt[0] * rg[0];
+        for (int s = 0; s < NR; ++s)
 #pragma unroll
-          for (int a = 1; a < Q; ++a) acc = fma(gt[a], rg[a], acc);
+          for (int a = 0; a < Q; ++a) rv[h][s][a] = in[s * D * D * LQ + a];
+        g[h] = gslot + e * G::GS + v * D;
+      }
 #pragma unroll
-          for (int a = 0; a < Q; ++a) acc = fma(bt[a], rb[a], acc);
-          atomicAdd(y + g[i], acc);
-        }
-      } else {
-        double rr[Q];
+      for (int i = 0; i < D; ++i) {
+        double bt[Q];
+        ld_row(tab + Tab::TBT + i * QP, bt);
+        if constexpr (NC == 3) {
+          double gt[Q];
+          ld_row(tab + Tab::TGT + i * QP, gt);
 #pragma unroll
-        for (int a = 0; a < Q; ++a) rr[a] = in[a];
+          for (int h = 0; h < NL; ++h) {
+            double acc = gt[0] * rv[h][0][0];
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-          double bt[Q];
-          ld_row(tab + TBT + i * QP, bt);
-          double acc = bt[0] * rr[0];
+            for (int a = 1; a < Q; ++a) acc = fma(gt[a], rv[h][0][a], acc);
 #pragma unroll
-          for (int a = 1; a < Q; ++a) acc = fma(bt[a], rr[a], acc);
-          atomicAdd(y + g[i], acc);
+            for (int a = 0; a < Q; ++a) acc = fma(bt[a], rv[h][1][a], acc);
+            if (ok[h]) atomicAdd(y + g[h][i], acc);
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < NL; ++h) {
+            double acc = bt[0] * rv[h][0][0];
+#pragma unroll
+            for (int a = 1; a < Q; ++a) acc = fma(bt[a], rv[h][0][a], acc);
+            if (ok[h]) atomicAdd(y + g[h][i], acc);
+          }
         }
       }
-    }
+    });
   }
 };
 

@@ -24,12 +24,11 @@ constexpr int round32(int n) { return ((n + 31) / 32) * 32; }
 // stage C (q^2 lines per element) is the heaviest: E*q^2 lines ~ 288
 constexpr int base_E(int Q) { return (288 / (Q * Q)) > 0 ? (288 / (Q * Q)) : 1; }
 
-template <int D, int Q, int NC, class Body>
+template <int D, int Q, int NC, class Body, bool PERSIST>
 void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
-  Tables<D, Q> tb;
-  std::memcpy(tb.B, v.B, sizeof(tb.B));
-  std::memcpy(tb.G, v.G, sizeof(tb.G));
-  pa_pipe_kernel<D, Q, NC, Body>
+  typename Body::Tab tb;
+  Body::fill(tb, v.B, v.G);
+  pa_pipe_kernel<D, Q, NC, Body, PERSIST>
       <<<blocks, Body::T, PipeSmem<D, Q, NC, Body::E, Body::EXTRA>::BYTES, s>>>(
           tb, x, y, v.gids, v.pa, v.ebits, v.nel);
 }
@@ -42,7 +41,7 @@ void launch_diag(const OpView& v, double* diag, int64_t nel, int blocks, cudaStr
   diagonal_kernel<D, Q, NC><<<blocks, 128, 0, s>>>(tb, diag, v.gids, v.pa, nel);
 }
 
-template <int D, int Q, int NC, class Body>
+template <int D, int Q, int NC, class Body, bool PERSIST = true>
 KernelEntry entry(int variant, int cfg) {
   KernelEntry k;
   k.nc = NC;
@@ -52,23 +51,34 @@ KernelEntry entry(int variant, int cfg) {
   k.cfg = cfg;
   k.E = Body::E;
   k.T = Body::T;
+  k.persist = PERSIST;
   k.smem = PipeSmem<D, Q, NC, Body::E, Body::EXTRA>::BYTES;
-  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body>);
-  k.launch = &launch_pipe<D, Q, NC, Body>;
+  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST>);
+  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST>;
   k.diag = &launch_diag<D, Q, NC>;
   return k;
 }
 
+// Compiled launch geometries (cfg index per variant; cfg 0 is the default).
+// Measured per order in the sweep (profiles/r01_sweep_*).
 template <int D, int Q, int NC>
 void add_all(std::vector<KernelEntry>& out) {
   constexpr int E0 = base_E(Q);
   constexpr int E1 = E0 / 2 > 0 ? E0 / 2 : 1;
   constexpr int E2 = E0 / 4 > 0 ? E0 / 4 : 1;
-  out.push_back(entry<D, Q, NC, DfmaBody<D, Q, NC, E1, round32(E1 * Q * Q)>>(FK_VARIANT_DFMA, 0));
-  out.push_back(entry<D, Q, NC, DfmaBody<D, Q, NC, E0, round32(E0 * Q * Q)>>(FK_VARIANT_DFMA, 1));
-  out.push_back(entry<D, Q, NC, DfmaBody<D, Q, NC, E2, round32(E2 * Q * Q)>>(FK_VARIANT_DFMA, 2));
-  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>>(FK_VARIANT_DMMA, 0));
-  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E0, 256>>(FK_VARIANT_DMMA, 1));
+  using F1 = DfmaBody<D, Q, NC, E1, round32(E1 * Q * Q), 1>;
+  using F2 = DfmaBody<D, Q, NC, E2, round32(E2 * Q * Q), 1>;
+  using F1x2 = DfmaBody<D, Q, NC, E1, round32((E1 * Q * Q + 1) / 2), 2>;
+  using F0x2 = DfmaBody<D, Q, NC, E0, round32((E0 * Q * Q + 1) / 2), 2>;
+  out.push_back(entry<D, Q, NC, F2, true>(FK_VARIANT_DFMA, 0));
+  out.push_back(entry<D, Q, NC, F1, true>(FK_VARIANT_DFMA, 1));
+  out.push_back(entry<D, Q, NC, F2, false>(FK_VARIANT_DFMA, 2));
+  out.push_back(entry<D, Q, NC, F1, false>(FK_VARIANT_DFMA, 3));
+  out.push_back(entry<D, Q, NC, F1x2, false>(FK_VARIANT_DFMA, 4));
+  out.push_back(entry<D, Q, NC, F0x2, false>(FK_VARIANT_DFMA, 5));
+  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true>(FK_VARIANT_DMMA, 0));
+  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E0, 256>, true>(FK_VARIANT_DMMA, 1));
+  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, false>(FK_VARIANT_DMMA, 2));
 }
 
 }  // namespace

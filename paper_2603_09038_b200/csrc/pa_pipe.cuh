@@ -38,8 +38,8 @@ struct PipeSmem {
   static constexpr size_t BYTES = OFF_EX + 8ull * EXTRA;
 };
 
-template <int D, int Q, int NC, class Body>
-__global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ Tables<D, Q> tb,
+template <int D, int Q, int NC, class Body, bool PERSIST>
+__global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ typename Body::Tab tb,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
                                                           const int* __restrict__ gids,
@@ -71,6 +71,11 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     mbar_init(bar_g + 1, 1);
     fence_mbar_init();
   }
+  // zero the work regions once: line padding stays finite (the DMMA body reads
+  // K padding and relies on zero B-operand rows to annihilate it)
+  for (size_t i = threadIdx.x; i < (S::BYTES - S::OFF_S0) / 8; i += T)
+    reinterpret_cast<double*>(smem_raw + S::OFF_S0)[i] = 0.0;
+  __syncthreads();
   Body::init(tb, ex);
   __syncthreads();
 
@@ -119,26 +124,24 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   ph_g0 ^= 1;
   issue_x(blockIdx.x, 0);
 
-  int it = 0;
-  for (int b = blockIdx.x; b < nbatch; b += gridDim.x, ++it) {
+  auto run_batch = [&](int b, int it, bool has_next) {
     const int slot = it & 1;
     const int e0 = b * E, ne = min(E, nel - e0);
     const int nb = b + gridDim.x;
-    const bool has_next = nb < nbatch;
     finish_x(slot, ne);
     __syncthreads();
 
-    Body::stage_a(tb, xb, s1, ne, ex);
+    Body::stage_a(tb, it, xb, s1, ne, ex);
     __syncthreads();
     if (has_next && threadIdx.x == 0) {
       fence_proxy_async();
       issue_g(nb, slot ^ 1);
     }
-    Body::stage_b(tb, s1, s0, ne, ex);
+    Body::stage_b(tb, it, s1, s0, ne, ex);
     __syncthreads();
     mbar_wait(bar_d, ph_d);
     ph_d ^= 1;
-    Body::stage_c(tb, s0, db, s1, ne, ex);
+    Body::stage_c(tb, it, s0, db, s1, ne, ex);
     __syncthreads();
     if (has_next) {
       if (threadIdx.x == 0) {
@@ -154,10 +157,20 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
       }
       issue_x(nb, slot ^ 1);
     }
-    Body::stage_d(tb, s1, s0, ne, ex);
+    Body::stage_d(tb, it, s1, s0, ne, ex);
     __syncthreads();
-    Body::stage_e(tb, s0, gs + slot * E * G::GS, y, ne, ex);
+    Body::stage_e(tb, it, s0, gs + slot * E * G::GS, y, ne, ex);
     __syncthreads();
+  };
+
+  if constexpr (PERSIST) {
+    int it = 0;
+    for (int b = blockIdx.x; b < nbatch; b += gridDim.x, ++it)
+      run_batch(b, it, b + (int)gridDim.x < nbatch);
+  } else {
+    // one batch per CTA: no loop, so the compiler has nothing to hoist the
+    // basis-table loads out of (co-resident CTAs overlap load and compute)
+    run_batch(blockIdx.x, 0, false);
   }
 }
 

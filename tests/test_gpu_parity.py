@@ -117,7 +117,7 @@ def test_apply_matches_oracle_all_orders(variant, kind, p, qoff):
     assert normwise(y, P.apply(x)) <= PARITY_TOL
 
 
-LAUNCH_CONFIGS = [("dfma", 0), ("dfma", 1), ("dfma", 2), ("dmma", 0), ("dmma", 1)]
+LAUNCH_CONFIGS = [("dfma", c) for c in range(6)] + [("dmma", c) for c in range(4)]
 
 
 @pytest.mark.parametrize("variant,cfg", LAUNCH_CONFIGS)
