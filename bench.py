@@ -43,11 +43,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kind", default="diffusion", choices=["diffusion", "mass"])
-    ap.add_argument("--p", type=int, default=4)
+    ap.add_argument("--p", type=int, default=None, help="order (default 4; 6 for --cg strong)")
     ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--n", type=int, default=None, help="elements per direction (per-rank slab is n^3)")
     ap.add_argument("--variant", default="auto", choices=["auto", "dfma", "dmma"])
     ap.add_argument("--sweep", default=None, help="also run the p=1..8 DFMA/DMMA sweep, JSON lines to FILE")
+    ap.add_argument("--cg", default=None, choices=["weak", "strong"],
+                    help="run the 100-iteration Jacobi-PCG benchmark (BASELINE configs[3]/[4])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -204,7 +206,7 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    p = a.p
+    p = a.p or 4
     q = a.q or p + 2
     n = a.n or SWEEP_N.get(p, 54)
     budget = max(1.0, min(5.0, 150.0 / max(1, a.steps + a.warmup)))
@@ -250,7 +252,7 @@ def run_ours(a):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = Comm(rank, world, local)
-    p = a.p
+    p = a.p or 4
     q = a.q or p + 2
     n = a.n or (54 if p == 4 else SWEEP_N.get(p, 54))
     mesh = build_mesh(n, n, n * world)
@@ -364,6 +366,70 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def run_cg(a):
+    """BASELINE configs[3]/[4]: 100-iteration Jacobi-PCG, homogeneous Dirichlet on
+    all faces, b ~ N(0,1) (seed = rank) with boundary entries zeroed, x0 = 0.
+    weak: p=4, 92^3 elements per GPU (z-slabs of a 92x92x(92N) box);
+    strong: p=6, fixed 98x98x96 box split into z-slabs.
+    Metric: GDOF/s = global dofs x iterations / solve time (MFEM BP convention);
+    the solve time includes the Jacobi-diagonal assembly (MAX over ranks)."""
+    import torch
+
+    from paper_2603_09038_b200 import Comm, PAOperator, build_mesh, cg_solve
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = Comm(rank, world, local)
+    if a.cg == "weak":
+        p, n = a.p or 4, a.n or 92
+        mesh, scaling = build_mesh(n, n, n * world), "weak"
+    else:
+        p, scaling = a.p or 6, "strong"
+        mesh = build_mesh(98, 98, 96) if a.n is None else build_mesh(a.n, a.n, a.n)
+    op = PAOperator(mesh, p, kind="diffusion", dirichlet=True, variant=a.variant, comm=comm)
+    b = torch.as_tensor(np.random.default_rng(rank).standard_normal(op.num_dofs), device="cuda")
+    op.set_essential(b, 0.0)
+    iters = 100
+    for _ in range(max(1, a.warmup // 3)):
+        cg_solve(op, b, iters=5)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    x, hist = cg_solve(op, b, iters=iters)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        ndof = op.num_global_dofs
+        print(json.dumps({
+            "metric": f"GDOF/s of BP3 Jacobi-PCG ({scaling} scaling, {iters} iterations)",
+            "value": ndof * iters / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
+            "ms_per_iteration": ms / iters, "ms_solve": ms, "iterations": len(hist) - 1,
+            "residual_0": float(hist[0]), "residual_final": float(hist[-1]),
+            "higher_is_better": True, "scaling": scaling, "dtype": "f64",
+            "config": {"workload": f"BP3 p={p} CG on {mesh.nx}x{mesh.ny}x{mesh.nz} ({ndof} dofs)",
+                       "p": p, "variant": op.variant, "dofs_per_gpu": op.num_dofs},
+        }), flush=True)
+    op.close()
+    if comm is not None:
+        comm.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def run_sweep(a, peak):
     """p=1..8 BP3/BP1 sweep, DFMA vs DMMA, written as JSON lines to a file."""
     import torch
@@ -405,6 +471,8 @@ def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.cg:
+        run_cg(a)
     else:
         run_ours(a)
 

@@ -118,6 +118,10 @@ int fk_op_apply_local(fk_op* op, const double* x_dev, double* y_dev);
 /* Assembled diagonal of A (Jacobi preconditioner); ones on essential dofs. */
 int fk_op_diagonal(fk_op* op, double* diag_dev);
 
+/* v[ess] = value on this rank's essential (Dirichlet) dofs (MFEM
+ * Vector::SetSubVector(ess_tdof_list, value)); no-op without dirichlet. */
+int fk_op_set_essential(fk_op* op, double* v_dev, double value);
+
 /* Jacobi-PCG (MFEM CGSolver semantics, x0 = 0), fixed `iters` iterations
  * unless rtol > 0 stops it (r.z <= rtol^2 r0.z0).  hist_host receives
  * sqrt(r_k . z_k) for k = 0..iters_done (iters+1 doubles).  Synchronises. */

@@ -36,6 +36,7 @@ EXPORTS = (
     "fk_op_get_info", "fk_op_set_variant", "fk_op_set_config", "fk_op_restriction",
     "fk_op_pa_data",
     "fk_op_apply", "fk_op_apply_host", "fk_op_apply_local", "fk_op_diagonal",
+    "fk_op_set_essential",
     "fk_cg_solve", "fk_dot", "fk_comm_unique_id", "fk_comm_create", "fk_comm_destroy",
     "fk_op_time_apply",
 )
@@ -121,6 +122,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "fk_op_apply_host": (i, [vp, vp, vp]),
         "fk_op_apply_local": (i, [vp, vp, vp]),
         "fk_op_diagonal": (i, [vp, vp]),
+        "fk_op_set_essential": (i, [vp, vp, d]),
         "fk_cg_solve": (i, [vp, vp, vp, i, d, pd, ctypes.POINTER(i)]),
         "fk_dot": (i, [vp, vp, vp, pd]),
         "fk_comm_unique_id": (i, [vp]),

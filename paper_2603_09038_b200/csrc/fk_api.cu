@@ -74,13 +74,23 @@ int grid_for(int64_t n, int threads, int num_sms) {
   return (int)std::max<int64_t>(1, std::min(b, cap));
 }
 
-// Per-order automatic variant (FK_VARIANT_AUTO), from the measured p-sweep
-// recorded in DESIGN.md ("variant choice").
+// Per-order automatic choice (FK_VARIANT_AUTO): variant and launch geometry
+// with the highest measured GDOF/s in the p-sweep on B200 (DESIGN.md §4.4,
+// profiles/r01_sweep_v5_noloop_pingpong.jsonl).  DFMA wins at every order on
+// sm_100a: DMMA and DFMA share the 37 TFLOP/s FP64 pipe, and DMMA's 8x8x4
+// padding wastes 14-88% of it at these shapes.
 int auto_variant(int nc, int p, int q) {
   (void)nc;
   (void)p;
   (void)q;
   return FK_VARIANT_DFMA;
+}
+
+int auto_cfg(int nc, int p) {
+  static const int bp3[9] = {0, 1, 1, 1, 0, 0, 0, 0, 1};
+  static const int bp1[9] = {0, 1, 1, 1, 1, 0, 0, 1, 3};
+  if (p < 1 || p > 8) return 0;
+  return nc == 3 ? bp3[p] : bp1[p];
 }
 
 fk::OpView view(const fk_op* op) {
@@ -98,6 +108,7 @@ int select_kernel(fk_op* op, int variant) {
   int v = variant == FK_VARIANT_AUTO ? auto_variant(op->nc, op->p, op->q) : variant;
   const fk::KernelEntry* k = nullptr;
   if (op->cfg >= 0) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, op->cfg);
+  else if (variant == FK_VARIANT_AUTO) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, auto_cfg(op->nc, op->p));
   if (k == nullptr) k = fk::find_kernel(op->nc, op->d, op->q, v);
   if (k == nullptr)
     return fail(FK_EUNSUPPORTED, "no %s kernel compiled for kind=%d p=%d q=%d",
@@ -484,6 +495,17 @@ int fk_op_diagonal(fk_op* op, double* diag) {
         diag, op->ess, op->n_ess, 1.0);
     FK_CUDA(cudaGetLastError());
   }
+  return FK_OK;
+}
+
+int fk_op_set_essential(fk_op* op, double* v, double value) {
+  if (op == nullptr || v == nullptr) return fail(FK_EINVAL, "null argument");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  if (!op->desc.dirichlet || op->n_ess == 0) return FK_OK;
+  DeviceGuard g(op->device);
+  fk::ess_set_kernel<<<grid_for(op->n_ess, 256, op->num_sms), 256, 0, op->stream>>>(v, op->ess,
+                                                                                    op->n_ess, value);
+  FK_CUDA(cudaGetLastError());
   return FK_OK;
 }
 

@@ -24,12 +24,12 @@ constexpr int round32(int n) { return ((n + 31) / 32) * 32; }
 // stage C (q^2 lines per element) is the heaviest: E*q^2 lines ~ 288
 constexpr int base_E(int Q) { return (288 / (Q * Q)) > 0 ? (288 / (Q * Q)) : 1; }
 
-template <int D, int Q, int NC, class Body, bool PERSIST>
+template <int D, int Q, int NC, class Body, bool PERSIST, bool DG>
 void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
   typename Body::Tab tb;
   Body::fill(tb, v.B, v.G);
-  pa_pipe_kernel<D, Q, NC, Body, PERSIST>
-      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body::E, Body::EXTRA>::BYTES, s>>>(
+  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG>
+      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body::E, Body::EXTRA, DG>::BYTES, s>>>(
           tb, x, y, v.gids, v.pa, v.ebits, v.nel);
 }
 
@@ -41,7 +41,7 @@ void launch_diag(const OpView& v, double* diag, int64_t nel, int blocks, cudaStr
   diagonal_kernel<D, Q, NC><<<blocks, 128, 0, s>>>(tb, diag, v.gids, v.pa, nel);
 }
 
-template <int D, int Q, int NC, class Body, bool PERSIST = true>
+template <int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false>
 KernelEntry entry(int variant, int cfg) {
   KernelEntry k;
   k.nc = NC;
@@ -52,9 +52,9 @@ KernelEntry entry(int variant, int cfg) {
   k.E = Body::E;
   k.T = Body::T;
   k.persist = PERSIST;
-  k.smem = PipeSmem<D, Q, NC, Body::E, Body::EXTRA>::BYTES;
-  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST>);
-  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST>;
+  k.smem = PipeSmem<D, Q, NC, Body::E, Body::EXTRA, DG>::BYTES;
+  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG>);
+  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG>;
   k.diag = &launch_diag<D, Q, NC>;
   return k;
 }
@@ -69,16 +69,15 @@ void add_all(std::vector<KernelEntry>& out) {
   using F1 = DfmaBody<D, Q, NC, E1, round32(E1 * Q * Q), 1>;
   using F2 = DfmaBody<D, Q, NC, E2, round32(E2 * Q * Q), 1>;
   using F1x2 = DfmaBody<D, Q, NC, E1, round32((E1 * Q * Q + 1) / 2), 2>;
-  using F0x2 = DfmaBody<D, Q, NC, E0, round32((E0 * Q * Q + 1) / 2), 2>;
   out.push_back(entry<D, Q, NC, F2, true>(FK_VARIANT_DFMA, 0));
   out.push_back(entry<D, Q, NC, F1, true>(FK_VARIANT_DFMA, 1));
-  out.push_back(entry<D, Q, NC, F2, false>(FK_VARIANT_DFMA, 2));
-  out.push_back(entry<D, Q, NC, F1, false>(FK_VARIANT_DFMA, 3));
-  out.push_back(entry<D, Q, NC, F1x2, false>(FK_VARIANT_DFMA, 4));
-  out.push_back(entry<D, Q, NC, F0x2, false>(FK_VARIANT_DFMA, 5));
+  out.push_back(entry<D, Q, NC, F2, true, true>(FK_VARIANT_DFMA, 2));   // D via L2, not smem
+  out.push_back(entry<D, Q, NC, F1, true, true>(FK_VARIANT_DFMA, 3));
+  out.push_back(entry<D, Q, NC, F1x2, true>(FK_VARIANT_DFMA, 4));       // 2 lines per thread
+  out.push_back(entry<D, Q, NC, F2, false>(FK_VARIANT_DFMA, 5));        // one batch per CTA
   out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true>(FK_VARIANT_DMMA, 0));
   out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E0, 256>, true>(FK_VARIANT_DMMA, 1));
-  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, false>(FK_VARIANT_DMMA, 2));
+  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true, true>(FK_VARIANT_DMMA, 2));
 }
 
 }  // namespace

@@ -1,14 +1,17 @@
 // pa_pipe.cuh — the persistent, software-pipelined fused PA kernel skeleton.
 //
 // One CTA owns batches b = blockIdx.x, blockIdx.x + gridDim.x, ... of E
-// elements.  While batch b is contracted, the next batch's inputs stream in
-// asynchronously, so no stage waits on HBM latency:
+// elements.  While batch b is contracted, the inputs of the next batches
+// stream in asynchronously, so no stage waits on HBM latency:
 //
-//   after stage A(b):  bulk copy (TMA engine) of the next batch's int32 gather
-//                      ids (+ Dirichlet bits) into the free smem slot
-//   after stage C(b):  bulk copy of the next batch's PA data D (the dominant
-//                      byte stream, 48 q^3 B per BP3 element) into smem, and
-//                      cp.async (LDGSTS) gathers x[gid] -> X buffer
+//   top of batch b:    x gather of batch b+1 (cp.async / LDGSTS, 8-byte
+//                      elements x[gid]) into the other X buffer — a whole
+//                      batch of compute hides its latency;
+//                      bulk copy (TMA engine, cp.async.bulk) of the int32
+//                      gather ids (+ Dirichlet bits) of batch b+2 into the
+//                      third gid slot
+//   after stage C(b):  bulk copy of batch b+1's PA data D (the dominant
+//                      byte stream, 48 q^3 B per BP3 element) into smem
 //   stage E(b):        atomic scatter-add (RED.F64) to y, fire-and-forget
 //
 // The contraction stages are supplied by Body (pa_dfma.cuh: FP64 FMA lines,
@@ -21,24 +24,28 @@
 
 namespace fk {
 
-template <int D, int Q, int NC, int E, int EXTRA>
+template <int D, int Q, int NC, int E, int EXTRA, bool DG = false>
 struct PipeSmem {
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
   static constexpr int XS = D * D * L::LS;  // X buffer doubles per element
+  static constexpr int NG = 3;              // gather-id slots (batches b, b+1, b+2)
   // byte offsets (16-byte aligned where bulk copies land)
-  static constexpr size_t OFF_BAR = 0;                                    // 3 mbarriers
-  static constexpr size_t OFF_DB = 32;                                    // PA data
-  static constexpr size_t OFF_GS = OFF_DB + 8ull * E * G::PS;             // 2 gid slots
-  static constexpr size_t OFF_MS = OFF_GS + 4ull * 2 * E * G::GS;         // 2 bit slots
-  static constexpr size_t OFF_S0 = OFF_MS + 4ull * 2 * E * G::MS;
+  static constexpr size_t OFF_BAR = 0;                                 // 4 mbarriers
+  static constexpr size_t OFF_DB = 32;                                 // PA data
+  static constexpr size_t OFF_GS = OFF_DB + (DG ? 0ull : 8ull * E * G::PS);  // NG gid slots
+  static constexpr size_t OFF_MS = OFF_GS + 4ull * NG * E * G::GS;     // NG bit slots
+  static constexpr size_t OFF_S0 = OFF_MS + 4ull * NG * E * G::MS;
   static constexpr size_t OFF_S1 = OFF_S0 + 8ull * E * L::P0;
-  static constexpr size_t OFF_XB = OFF_S1 + 8ull * E * L::P1;
-  static constexpr size_t OFF_EX = (OFF_XB + 8ull * E * XS + 15) / 16 * 16;
+  static constexpr size_t OFF_XB = OFF_S1 + 8ull * E * L::P1;         // 2 X buffers
+  static constexpr size_t OFF_EX = (OFF_XB + 8ull * 2 * E * XS + 15) / 16 * 16;
   static constexpr size_t BYTES = OFF_EX + 8ull * EXTRA;
 };
 
-template <int D, int Q, int NC, class Body, bool PERSIST>
+// DG (high orders, where E*48q^3 bytes of smem would cap occupancy): stage C
+// reads D straight from global memory; the next batch's D range is pulled
+// toward L2 with cp.async.bulk.prefetch.L2 instead of copied into smem.
+template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false>
 __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ typename Body::Tab tb,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
@@ -49,11 +56,11 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   constexpr int E = Body::E, T = Body::T;
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
-  using S = PipeSmem<D, Q, NC, E, Body::EXTRA>;
-  constexpr int D3 = L::D3, LS = L::LS, XS = S::XS;
+  using S = PipeSmem<D, Q, NC, E, Body::EXTRA, DG>;
+  constexpr int D3 = L::D3, LS = L::LS, XS = S::XS, NG = S::NG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar_d = reinterpret_cast<uint64_t*>(smem_raw + S::OFF_BAR);
-  uint64_t* bar_g = bar_d + 1;  // [2]
+  uint64_t* bar_g = bar_d + 1;  // [NG]
   double* db = reinterpret_cast<double*>(smem_raw + S::OFF_DB);
   int* gs = reinterpret_cast<int*>(smem_raw + S::OFF_GS);
   uint32_t* ms = reinterpret_cast<uint32_t*>(smem_raw + S::OFF_MS);
@@ -67,8 +74,8 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   const bool dirichlet = ebits != nullptr;
   if (threadIdx.x == 0) {
     mbar_init(bar_d, 1);
-    mbar_init(bar_g, 1);
-    mbar_init(bar_g + 1, 1);
+#pragma unroll
+    for (int s = 0; s < NG; ++s) mbar_init(bar_g + s, 1);
     fence_mbar_init();
   }
   // zero the work regions once: line padding stays finite (the DMMA body reads
@@ -89,88 +96,96 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   auto issue_d = [&](int b) {
     const int e0 = b * E, ne = min(E, nel - e0);
     const uint32_t bytes = 8u * ne * G::PS;
-    mbar_expect_tx(bar_d, bytes);
-    bulk_g2s(db, pa + (size_t)e0 * G::PS, bytes, bar_d);
+    if constexpr (DG) {
+      prefetch_l2(pa + (size_t)e0 * G::PS, bytes);
+    } else {
+      mbar_expect_tx(bar_d, bytes);
+      bulk_g2s(db, pa + (size_t)e0 * G::PS, bytes, bar_d);
+    }
   };
-  auto issue_x = [&](int b, int slot) {
+  auto issue_x = [&](int b, int gslot, double* xdst) {
     const int e0 = b * E, ne = min(E, nel - e0);
-    const int* g = gs + slot * E * G::GS;
+    const int* g = gs + gslot * E * G::GS;
     for (int t = threadIdx.x; t < E * D3; t += T) {
       const int e = t / D3, l = t - e * D3;
-      double* dst = xb + e * XS + (l / D) * LS + (l % D);
+      double* dst = xdst + e * XS + (l / D) * LS + (l % D);
       if (e < ne) cp_async8(dst, x + g[e * G::GS + l]);
       else *dst = 0.0;
     }
     cp_async_commit();
   };
-  auto finish_x = [&](int slot, int ne) {
+  auto finish_x = [&](int gslot, int ne, double* xsrc) {
     cp_async_wait_all();
     if (dirichlet) {
-      const uint32_t* m = ms + slot * E * G::MS;
+      const uint32_t* m = ms + gslot * E * G::MS;
       for (int t = threadIdx.x; t < ne * D3; t += T) {
         const int e = t / D3, l = t - e * D3;
-        if ((m[e * G::MS + (l >> 5)] >> (l & 31)) & 1u) xb[e * XS + (l / D) * LS + (l % D)] = 0.0;
+        if ((m[e * G::MS + (l >> 5)] >> (l & 31)) & 1u) xsrc[e * XS + (l / D) * LS + (l % D)] = 0.0;
       }
     }
   };
+  // mbarrier phase bits of the gid slots (bit s) and of the D barrier
+  uint32_t ph_g = 0u, ph_d = 0u;
+  auto wait_g = [&](int slot) {
+    mbar_wait(bar_g + slot, (ph_g >> slot) & 1u);
+    ph_g ^= 1u << slot;
+  };
 
-  uint32_t ph_d = 0, ph_g0 = 0, ph_g1 = 0;
-  // prologue: first batch
+  const int stride = PERSIST ? (int)gridDim.x : nbatch;  // single-batch CTAs never see a next
+  // prologue: ids of the first two batches, D of the first, x of the first
   if (threadIdx.x == 0) {
     issue_g(blockIdx.x, 0);
+    if (blockIdx.x + stride < nbatch) issue_g(blockIdx.x + stride, 1);
     issue_d(blockIdx.x);
   }
-  mbar_wait(bar_g, ph_g0);
-  ph_g0 ^= 1;
-  issue_x(blockIdx.x, 0);
+  wait_g(0);
+  issue_x(blockIdx.x, 0, xb);
 
-  auto run_batch = [&](int b, int it, bool has_next) {
-    const int slot = it & 1;
+  auto run_batch = [&](int b, int it) {
+    const int gslot = it % NG;
+    double* xcur = xb + (it & 1) * E * XS;
+    double* xnext = xb + ((it + 1) & 1) * E * XS;
     const int e0 = b * E, ne = min(E, nel - e0);
-    const int nb = b + gridDim.x;
-    finish_x(slot, ne);
+    const int nb = b + stride, nb2 = nb + stride;
+    finish_x(gslot, ne, xcur);
     __syncthreads();
-
-    Body::stage_a(tb, it, xb, s1, ne, ex);
-    __syncthreads();
-    if (has_next && threadIdx.x == 0) {
-      fence_proxy_async();
-      issue_g(nb, slot ^ 1);
+    if (nb < nbatch) {
+      wait_g((it + 1) % NG);
+      issue_x(nb, (it + 1) % NG, xnext);
+      if (nb2 < nbatch && threadIdx.x == 0) {
+        fence_proxy_async();
+        issue_g(nb2, (it + 2) % NG);  // slot last read by batch b-1 (done)
+      }
     }
+    Body::stage_a(tb, it, xcur, s1, ne, ex);
+    __syncthreads();
     Body::stage_b(tb, it, s1, s0, ne, ex);
     __syncthreads();
-    mbar_wait(bar_d, ph_d);
-    ph_d ^= 1;
-    Body::stage_c(tb, it, s0, db, s1, ne, ex);
+    if constexpr (DG) {
+      Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, s1, ne, ex);
+    } else {
+      mbar_wait(bar_d, ph_d);
+      ph_d ^= 1u;
+      Body::stage_c(tb, it, s0, db, s1, ne, ex);
+    }
     __syncthreads();
-    if (has_next) {
-      if (threadIdx.x == 0) {
-        fence_proxy_async();
-        issue_d(nb);
-      }
-      if (slot == 0) {
-        mbar_wait(bar_g + 1, ph_g1);
-        ph_g1 ^= 1;
-      } else {
-        mbar_wait(bar_g, ph_g0);
-        ph_g0 ^= 1;
-      }
-      issue_x(nb, slot ^ 1);
+    if (nb < nbatch && threadIdx.x == 0) {
+      fence_proxy_async();
+      issue_d(nb);
     }
     Body::stage_d(tb, it, s1, s0, ne, ex);
     __syncthreads();
-    Body::stage_e(tb, it, s0, gs + slot * E * G::GS, y, ne, ex);
+    Body::stage_e(tb, it, s0, gs + gslot * E * G::GS, y, ne, ex);
     __syncthreads();
   };
 
   if constexpr (PERSIST) {
     int it = 0;
-    for (int b = blockIdx.x; b < nbatch; b += gridDim.x, ++it)
-      run_batch(b, it, b + (int)gridDim.x < nbatch);
+    for (int b = blockIdx.x; b < nbatch; b += gridDim.x, ++it) run_batch(b, it);
   } else {
     // one batch per CTA: no loop, so the compiler has nothing to hoist the
     // basis-table loads out of (co-resident CTAs overlap load and compute)
-    run_batch(blockIdx.x, 0, false);
+    run_batch(blockIdx.x, 0);
   }
 }
 

@@ -304,6 +304,12 @@ class PAOperator:
         _lib.check(self._lib.fk_op_diagonal(self._h, d.data_ptr()))
         return d
 
+    def set_essential(self, v, value: float = 0.0):
+        """v[ess] = value on this rank's Dirichlet dofs (in place)."""
+        self._dev(v, "v")
+        _lib.check(self._lib.fk_op_set_essential(self._h, v.data_ptr(), float(value)))
+        return v
+
     def dot(self, a, b) -> float:
         """Global (all-rank) dot product over owned dofs."""
         self._dev(a, "a")
