@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--p", type=int, default=None, help="order (default 4; 6 for --cg strong)")
     ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--n", type=int, default=None, help="elements per direction (per-rank slab is n^3)")
-    ap.add_argument("--variant", default="auto", choices=["auto", "dfma", "dmma"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "dfma", "dmma", "eo"])
     ap.add_argument("--sweep", default=None, help="also run the p=1..8 DFMA/DMMA sweep, JSON lines to FILE")
     ap.add_argument("--cg", default=None, choices=["weak", "strong"],
                     help="run the 100-iteration Jacobi-PCG benchmark (BASELINE configs[3]/[4])")
@@ -443,7 +443,8 @@ def run_sweep(a, peak):
             op = PAOperator(build_mesh(n, n, n), p, kind=kind)
             x = torch.randn(op.num_dofs, dtype=torch.float64, device="cuda")
             y = torch.empty_like(x)
-            for variant, cfg in [("dfma", c) for c in range(6)] + [("dmma", c) for c in range(4)]:
+            for variant, cfg in ([("dfma", c) for c in range(6)] + [("dmma", c) for c in range(4)]
+                                 + [("eo", c) for c in range(4)]):
                 try:
                     op.set_config(variant, cfg)
                 except NotImplementedError:

@@ -46,6 +46,9 @@ extern "C" {
 #define FK_VARIANT_AUTO 0   /* per-order choice from the measured sweep */
 #define FK_VARIANT_DFMA 1   /* register-blocked FP64 FMA, basis in the constant bank */
 #define FK_VARIANT_DMMA 2   /* warp mma.sync.m8n8k4 f64 tiles (DMMA.8x8x4)           */
+#define FK_VARIANT_EO 3     /* FP64 FMA with even-odd folding of the symmetric 1D tables
+                               (half the multiply-adds; symmetric bases only)         */
+#define FK_VARIANT_LAST FK_VARIANT_EO
 
 typedef struct fk_op fk_op;
 typedef struct fk_comm fk_comm;

@@ -27,7 +27,10 @@ FK_VARIANT_AUTO = 0
 FK_VARIANT_DFMA = 1
 FK_VARIANT_DMMA = 2
 
-VARIANTS = {"auto": FK_VARIANT_AUTO, "dfma": FK_VARIANT_DFMA, "dmma": FK_VARIANT_DMMA}
+FK_VARIANT_EO = 3
+
+VARIANTS = {"auto": FK_VARIANT_AUTO, "dfma": FK_VARIANT_DFMA, "dmma": FK_VARIANT_DMMA,
+            "eo": FK_VARIANT_EO}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 
 #: every symbol include/fk.h declares (checked by tests/test_cabi.py)

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -87,8 +88,8 @@ int auto_variant(int nc, int p, int q) {
 }
 
 int auto_cfg(int nc, int p) {
-  static const int bp3[9] = {0, 1, 1, 1, 0, 0, 0, 0, 1};
-  static const int bp1[9] = {0, 1, 1, 1, 1, 0, 0, 1, 3};
+  static const int bp3[9] = {0, 1, 1, 1, 0, 2, 2, 2, 2};
+  static const int bp1[9] = {0, 3, 1, 1, 0, 1, 0, 3, 5};
   if (p < 1 || p > 8) return 0;
   return nc == 3 ? bp3[p] : bp1[p];
 }
@@ -104,15 +105,36 @@ fk::OpView view(const fk_op* op) {
   return v;
 }
 
+// Even-odd folding needs B[q-1-a][d-1-i] = B[a][i] and G[q-1-a][d-1-i] = -G[a][i]
+// (symmetric nodes and points, as Basis1D.nodal produces, tensor.py:101-119).
+bool tables_symmetric(const fk_op* op) {
+  const int d = op->d, q = op->q;
+  double mb = 0.0, mg = 0.0, eb = 0.0, eg = 0.0;
+  for (int a = 0; a < q; ++a)
+    for (int i = 0; i < d; ++i) {
+      mb = std::max(mb, std::fabs(op->B[a * d + i]));
+      mg = std::max(mg, std::fabs(op->G[a * d + i]));
+      eb = std::max(eb, std::fabs(op->B[a * d + i] - op->B[(q - 1 - a) * d + (d - 1 - i)]));
+      eg = std::max(eg, std::fabs(op->G[a * d + i] + op->G[(q - 1 - a) * d + (d - 1 - i)]));
+    }
+  return eb <= 1e-12 * mb && eg <= 1e-12 * mg;
+}
+
 int select_kernel(fk_op* op, int variant) {
   int v = variant == FK_VARIANT_AUTO ? auto_variant(op->nc, op->p, op->q) : variant;
+  if (v == FK_VARIANT_EO && !tables_symmetric(op)) {
+    if (variant != FK_VARIANT_AUTO)
+      return fail(FK_EUNSUPPORTED, "even-odd variant needs symmetric basis tables");
+    v = FK_VARIANT_DFMA;
+  }
   const fk::KernelEntry* k = nullptr;
   if (op->cfg >= 0) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, op->cfg);
   else if (variant == FK_VARIANT_AUTO) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, auto_cfg(op->nc, op->p));
   if (k == nullptr) k = fk::find_kernel(op->nc, op->d, op->q, v);
   if (k == nullptr)
     return fail(FK_EUNSUPPORTED, "no %s kernel compiled for kind=%d p=%d q=%d",
-                v == FK_VARIANT_DMMA ? "DMMA" : "DFMA", op->desc.kind, op->p, op->q);
+                v == FK_VARIANT_DMMA ? "DMMA" : v == FK_VARIANT_EO ? "even-odd" : "DFMA",
+                op->desc.kind, op->p, op->q);
   {
     int max_smem = 0;
     DeviceGuard g(op->device);
@@ -235,7 +257,7 @@ int fk_op_create(fk_op** out, const fk_op_desc* d) {
     return fail(FK_EINVAL, "non-positive Jacobian");
   if (d->B == nullptr || d->G == nullptr || d->w == nullptr)
     return fail(FK_EINVAL, "basis tables B, G, w are required");
-  if (d->variant < FK_VARIANT_AUTO || d->variant > FK_VARIANT_DMMA)
+  if (d->variant < FK_VARIANT_AUTO || d->variant > FK_VARIANT_LAST)
     return fail(FK_EINVAL, "unknown variant %d", d->variant);
 
   fk_op* op = new fk_op();
@@ -406,15 +428,16 @@ int fk_op_get_info(const fk_op* op, fk_op_info* info) {
 
 int fk_op_set_variant(fk_op* op, int variant) {
   if (op == nullptr) return fail(FK_EINVAL, "null handle");
-  if (variant < FK_VARIANT_AUTO || variant > FK_VARIANT_DMMA)
+  if (variant < FK_VARIANT_AUTO || variant > FK_VARIANT_LAST)
     return fail(FK_EINVAL, "unknown variant %d", variant);
   op->desc.variant = variant;
+  op->cfg = -1;
   return select_kernel(op, variant);
 }
 
 int fk_op_set_config(fk_op* op, int variant, int cfg) {
   if (op == nullptr) return fail(FK_EINVAL, "null handle");
-  if (variant < FK_VARIANT_DFMA || variant > FK_VARIANT_DMMA || cfg < 0)
+  if (variant < FK_VARIANT_DFMA || variant > FK_VARIANT_LAST || cfg < 0)
     return fail(FK_EINVAL, "bad variant %d / cfg %d", variant, cfg);
   if (fk::find_kernel_cfg(op->nc, op->d, op->q, variant, cfg) == nullptr)
     return fail(FK_EUNSUPPORTED, "no launch config %d for variant %d", cfg, variant);

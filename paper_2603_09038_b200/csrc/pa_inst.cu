@@ -10,6 +10,7 @@
 #include "fk_internal.h"
 #include "pa_diag.cuh"
 #include "pa_dfma.cuh"
+#include "pa_dfma_eo.cuh"
 #include "pa_dmma.cuh"
 #include "pa_pipe.cuh"
 
@@ -78,6 +79,12 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true>(FK_VARIANT_DMMA, 0));
   out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E0, 256>, true>(FK_VARIANT_DMMA, 1));
   out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true, true>(FK_VARIANT_DMMA, 2));
+  using O1 = DfmaEoBody<D, Q, NC, E1, round32(E1 * Q * Q)>;
+  using O2 = DfmaEoBody<D, Q, NC, E2, round32(E2 * Q * Q)>;
+  out.push_back(entry<D, Q, NC, O2, true>(FK_VARIANT_EO, 0));
+  out.push_back(entry<D, Q, NC, O1, true>(FK_VARIANT_EO, 1));
+  out.push_back(entry<D, Q, NC, O2, true, true>(FK_VARIANT_EO, 2));
+  out.push_back(entry<D, Q, NC, O1, true, true>(FK_VARIANT_EO, 3));
 }
 
 }  // namespace

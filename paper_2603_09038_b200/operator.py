@@ -221,8 +221,8 @@ class PAOperator:
 
     def set_config(self, variant: str, cfg: int) -> None:
         """Pick compiled launch geometry ``cfg`` of ``variant`` ("dfma"/"dmma")."""
-        if variant not in ("dfma", "dmma"):
-            raise ValueError(f"variant must be 'dfma' or 'dmma', got {variant!r}")
+        if variant not in ("dfma", "dmma", "eo"):
+            raise ValueError(f"variant must be 'dfma', 'dmma' or 'eo', got {variant!r}")
         _lib.check(self._lib.fk_op_set_config(self._h, _lib.VARIANTS[variant], int(cfg)))
         self.info = self._info()
 

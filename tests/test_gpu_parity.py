@@ -34,7 +34,7 @@ def dev(x):
     return torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda")
 
 
-VARIANTS = ["dfma", "dmma"]
+VARIANTS = ["dfma", "dmma", "eo"]
 
 GOLDEN_CASES = (
     [("mass", (8, 8, 8), 2, None, (1.0, 1.0, 1.0), "bp1_8x8x8_p2")]
@@ -117,7 +117,8 @@ def test_apply_matches_oracle_all_orders(variant, kind, p, qoff):
     assert normwise(y, P.apply(x)) <= PARITY_TOL
 
 
-LAUNCH_CONFIGS = [("dfma", c) for c in range(6)] + [("dmma", c) for c in range(4)]
+LAUNCH_CONFIGS = ([("dfma", c) for c in range(6)] + [("dmma", c) for c in range(4)]
+                  + [("eo", c) for c in range(4)])
 
 
 @pytest.mark.parametrize("variant,cfg", LAUNCH_CONFIGS)
