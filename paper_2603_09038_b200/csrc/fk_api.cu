@@ -80,18 +80,22 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // profiles/r01_sweep_v5_noloop_pingpong.jsonl).  DFMA wins at every order on
 // sm_100a: DMMA and DFMA share the 37 TFLOP/s FP64 pipe, and DMMA's 8x8x4
 // padding wastes 14-88% of it at these shapes.
+// (variant, cfg) per order, best of profiles/r01_sweep_v7_eo.jsonl
+constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
+const int kAutoVar3[9] = {D_, O_, D_, O_, O_, O_, D_, O_, D_};
+const int kAutoCfg3[9] = {0, 1, 1, 1, 0, 0, 2, 3, 2};
+const int kAutoVar1[9] = {D_, D_, D_, D_, O_, O_, O_, O_, O_};
+const int kAutoCfg1[9] = {0, 3, 1, 1, 1, 1, 0, 1, 1};
+
 int auto_variant(int nc, int p, int q) {
-  (void)nc;
-  (void)p;
   (void)q;
-  return FK_VARIANT_DFMA;
+  if (p < 1 || p > 8) return FK_VARIANT_DFMA;
+  return nc == 3 ? kAutoVar3[p] : kAutoVar1[p];
 }
 
 int auto_cfg(int nc, int p) {
-  static const int bp3[9] = {0, 1, 1, 1, 0, 2, 2, 2, 2};
-  static const int bp1[9] = {0, 3, 1, 1, 0, 1, 0, 3, 5};
   if (p < 1 || p > 8) return 0;
-  return nc == 3 ? bp3[p] : bp1[p];
+  return nc == 3 ? kAutoCfg3[p] : kAutoCfg1[p];
 }
 
 fk::OpView view(const fk_op* op) {
@@ -163,6 +167,7 @@ int select_kernel(fk_op* op, int variant) {
     FK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->func, k->T, k->smem));
     if (occ < 1) return fail(FK_EUNSUPPORTED, "fused kernel does not fit on an SM (smem %zu)", k->smem);
     const int64_t nbatch = (op->nel + k->E - 1) / k->E;
+    op->max_blocks = occ * op->num_sms;
     op->blocks = k->persist
                      ? (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ * op->num_sms))
                      : (int)std::max<int64_t>(1, nbatch);
@@ -408,6 +413,10 @@ int fk_op_destroy(fk_op* op) {
   if (op->ev2) cudaEventDestroy(op->ev2);
   if (op->ev3) cudaEventDestroy(op->ev3);
   if (op->cg_stream) cudaStreamDestroy(op->cg_stream);
+  if (op->h2d) cudaStreamDestroy(op->h2d);
+  if (op->d2h) cudaStreamDestroy(op->d2h);
+  for (auto& e : op->chunk_ev)
+    if (e) cudaEventDestroy(e);
   delete op;
   return FK_OK;
 }
@@ -495,10 +504,56 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
     FK_CUDA(cudaMalloc(&op->stage_x, bytes));
     FK_CUDA(cudaMalloc(&op->stage_y, bytes));
   }
-  FK_CUDA(cudaMemcpyAsync(op->stage_x, xh, bytes, cudaMemcpyHostToDevice, op->stream));
-  FK_TRY(apply_full(op, op->stage_x, op->stage_y));
-  FK_CUDA(cudaMemcpyAsync(yh, op->stage_y, bytes, cudaMemcpyDeviceToHost, op->stream));
-  FK_CUDA(cudaStreamSynchronize(op->stream));
+  const int nzl = op->desc.nz_local;
+  if (op->comm != nullptr || op->desc.dirichlet || nzl < 4 || op->kern == nullptr) {
+    FK_CUDA(cudaMemcpyAsync(op->stage_x, xh, bytes, cudaMemcpyHostToDevice, op->stream));
+    FK_TRY(apply_full(op, op->stage_x, op->stage_y));
+    FK_CUDA(cudaMemcpyAsync(yh, op->stage_y, bytes, cudaMemcpyDeviceToHost, op->stream));
+    FK_CUDA(cudaStreamSynchronize(op->stream));
+    return FK_OK;
+  }
+  // z-chunk pipeline: chunk c's x planes go up while chunk c-1 computes and the
+  // completed y planes of chunk c-2 come down (PCIe is full duplex).  Dof
+  // planes are z-slowest (mesh.py:164): chunk of element layers [z0, z1) reads
+  // planes [z0 p, z1 p] and finalises every plane below z1 p.
+  if (op->h2d == nullptr) {
+    FK_CUDA(cudaStreamCreateWithFlags(&op->h2d, cudaStreamNonBlocking));
+    FK_CUDA(cudaStreamCreateWithFlags(&op->d2h, cudaStreamNonBlocking));
+    for (auto& e : op->chunk_ev) FK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int K = std::min(nzl, 8);
+  const int64_t P = op->npx * op->npy, nxy = (int64_t)op->desc.nx * op->desc.ny;
+  const int p = op->p;
+  FK_CUDA(cudaEventRecord(op->chunk_ev[30], op->stream));  // order after prior work
+  FK_CUDA(cudaStreamWaitEvent(op->h2d, op->chunk_ev[30], 0));
+  FK_CUDA(cudaMemsetAsync(op->stage_y, 0, bytes, op->stream));
+  int64_t x_done = 0, y_done = 0;
+  for (int c = 0; c < K; ++c) {
+    const int z0 = (int)((int64_t)nzl * c / K), z1 = (int)((int64_t)nzl * (c + 1) / K);
+    const int64_t x_hi = (int64_t)z1 * p + 1;
+    FK_CUDA(cudaMemcpyAsync(op->stage_x + x_done * P, xh + x_done * P,
+                            sizeof(double) * (x_hi - x_done) * P, cudaMemcpyHostToDevice, op->h2d));
+    x_done = x_hi;
+    FK_CUDA(cudaEventRecord(op->chunk_ev[2 * c], op->h2d));
+    FK_CUDA(cudaStreamWaitEvent(op->stream, op->chunk_ev[2 * c], 0));
+    fk::OpView v = view(op);
+    const int64_t e0 = (int64_t)z0 * nxy, ne = (int64_t)(z1 - z0) * nxy;
+    v.gids += e0 * op->gs;
+    v.pa += e0 * op->ps;
+    v.nel = (int)ne;
+    const int64_t nb = (ne + op->kern->E - 1) / op->kern->E;
+    const int blocks = (int)std::max<int64_t>(
+        1, op->kern->persist ? std::min<int64_t>(nb, op->max_blocks) : nb);
+    op->kern->launch(v, op->stage_x, op->stage_y, blocks, op->stream);
+    FK_CUDA(cudaGetLastError());
+    FK_CUDA(cudaEventRecord(op->chunk_ev[2 * c + 1], op->stream));
+    FK_CUDA(cudaStreamWaitEvent(op->d2h, op->chunk_ev[2 * c + 1], 0));
+    const int64_t y_hi = (c == K - 1) ? op->npz_local : (int64_t)z1 * p;
+    FK_CUDA(cudaMemcpyAsync(yh + y_done * P, op->stage_y + y_done * P,
+                            sizeof(double) * (y_hi - y_done) * P, cudaMemcpyDeviceToHost, op->d2h));
+    y_done = y_hi;
+  }
+  FK_CUDA(cudaStreamSynchronize(op->d2h));
   return FK_OK;
 }
 

@@ -75,9 +75,12 @@ struct fk_op {
   int cfg = -1;                    // launch-geometry override (FK_CFG)
   int* ess = nullptr;
   int64_t n_ess = 0;
-  // host staging for fk_op_apply_host
+  // host staging for fk_op_apply_host (z-chunk pipeline: H2D / compute / D2H)
   double* stage_x = nullptr;
   double* stage_y = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t chunk_ev[32] = {};
+  int max_blocks = 0;  // resident CTAs of the fused kernel on the device
   // CG / reduction workspace
   double* work = nullptr;  // r, z, p, Ap, dinv (5 * ndof)
   double* scal = nullptr;  // scalars
