@@ -209,6 +209,64 @@ def test_host_buffers_chunk_pipeline(kind, n, p):
     assert normwise(op.apply(x), P.apply(x)) <= PARITY_TOL
 
 
+@pytest.mark.parametrize("kind,n,p,world", [("diffusion", (4, 3, 7), 3, 3), ("mass", (3, 3, 4), 5, 2),
+                                             ("diffusion", (5, 5, 8), 4, 4)])
+@pytest.mark.parametrize("dirichlet", [False, True])
+def test_zslab_loopback_matches_single_gpu(kind, n, p, world, dirichlet):
+    """The multi-GPU decomposition on one device: every rank's z-slab operator
+    (local restriction offsets, slab Dirichlet faces) applied element-locally,
+    interface planes summed by hand (what fk_comm.cu does over NCCL), then the
+    Dirichlet copy — must equal the single-GPU / oracle apply."""
+    from paper_2603_09038_b200 import parallel
+
+    nx, ny, nz = n
+    P = bp.Problem(kind, *n, p)
+    x = np.random.default_rng(11).standard_normal(P.ndof)
+    ref = P.constrained_apply(x, P.boundary()) if dirichlet else P.apply(x)
+    plane = parallel.plane_size(nx, ny, p)
+    parts = []
+    for r in range(world):
+        z0, z1 = parallel.slab_range(nz, r, world)
+        op = make(kind, n, p, z_range=(z0, z1), dirichlet=dirichlet)
+        s, e = parallel.local_dof_range(nx, ny, p, z0, z1)
+        assert op.dof_offset == s and op.num_dofs == e - s
+        assert np.array_equal(op.restriction_ids(), bp.gather_ids(nx, ny, nz, p + 1, (z0, z1)))
+        xl = dev(x[s:e])
+        if dirichlet:
+            xl = op.set_essential(xl.clone(), 0.0)
+        parts.append((op, s, e, op.apply_local(xl).cpu().numpy()))
+    y = np.zeros(P.ndof)
+    for op, s, e, yl in parts:
+        y[s:e] += yl  # shared planes receive both partial sums
+    if dirichlet:
+        ess = P.boundary()
+        y[ess] = x[ess]
+    assert normwise(y, ref) <= PARITY_TOL
+
+
+def test_comm_single_rank_path():
+    """fk_comm_create through the dlopen'ed NCCL (the copy torch loaded) with one
+    rank: exchange and allreduce are no-ops, results unchanged."""
+    import torch.distributed as dist
+
+    from paper_2603_09038_b200 import Comm
+
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29577", rank=0, world_size=1)
+    comm = Comm(0, 1, 0)
+    op = make("diffusion", (3, 3, 4), 3, dirichlet=True, comm=comm)
+    ref = make("diffusion", (3, 3, 4), 3, dirichlet=True)
+    x = dev(np.random.default_rng(2).standard_normal(op.num_dofs))
+    assert normwise(op.apply(x).cpu().numpy(), ref.apply(x).cpu().numpy()) <= 1e-15
+    b = ref.set_essential(dev(np.random.default_rng(3).standard_normal(op.num_dofs)), 0.0)
+    _, h1 = cg_solve(op, b, iters=30)
+    _, h2 = cg_solve(ref, b, iters=30)
+    assert np.max(np.abs(h1 - h2)) <= 1e-10 * h2[0]
+    op.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def test_mass_integrates_volume():
     for ext in ((1.0, 1.0, 1.0), (2.0, 1.0, 0.5)):
         op = make("mass", (4, 3, 5), 5, ext=ext)
