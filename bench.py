@@ -340,8 +340,10 @@ def run_ours(a):
                        "mesh": [n, n, n * world], "p": p, "q": q,
                        "elements_per_gpu": n ** 3, "dofs_per_gpu": op.num_dofs,
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
-                       "variant": op.variant, "l2": "inputs larger than L2 (PA data "
-                       f"{op.info.pa_bytes / 1e9:.2f} GB per apply)",
+                       "variant": op.variant,
+                       "l2": (f"inputs larger than L2 (PA data {op.info.pa_bytes / 1e9:.2f} GB "
+                              "per apply, no flush needed)" if op.bytes_per_apply > 126e6 else
+                              "small config: L2-resident between steps (not a bandwidth number)"),
                        "launch": {"elems_per_block": op.info.elems_per_block,
                                   "threads": op.info.threads_per_block, "blocks": op.info.blocks}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
