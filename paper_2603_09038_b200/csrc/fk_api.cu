@@ -182,11 +182,50 @@ int launch_local(fk_op* op, const double* x, double* y) {
   return FK_OK;
 }
 
+// Fused kernel over local elements [e0, e0 + ne) (gids / PA data offset views).
+int launch_range(fk_op* op, const double* x, double* y, int64_t e0, int64_t ne, cudaStream_t s) {
+  if (ne <= 0) return FK_OK;
+  fk::OpView v = view(op);
+  v.gids += e0 * op->gs;
+  v.pa += e0 * op->ps;
+  if (v.ebits) v.ebits += e0 * op->ms;
+  v.nel = (int)ne;
+  const int64_t nb = (ne + op->kern->E - 1) / op->kern->E;
+  const int blocks =
+      (int)std::max<int64_t>(1, op->kern->persist ? std::min<int64_t>(nb, op->max_blocks) : nb);
+  op->kern->launch(v, x, y, blocks, s);
+  FK_CUDA(cudaGetLastError());
+  return FK_OK;
+}
+
+// Multi-rank apply with the interface exchange overlapped:
+// boundary element layers first, then the NCCL plane swap on the comm stream
+// runs while the interior layers (which never touch an interface plane)
+// compute; the received partial sums are added after the join.
+int apply_overlapped(fk_op* op, const double* x, double* y) {
+  const int64_t nxy = (int64_t)op->desc.nx * op->desc.ny;
+  FK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * op->ndof, op->stream));
+  FK_TRY(launch_range(op, x, y, 0, nxy, op->stream));
+  FK_TRY(launch_range(op, x, y, op->nel - nxy, nxy, op->stream));
+  FK_CUDA(cudaEventRecord(op->ev_bnd, op->stream));
+  FK_CUDA(cudaStreamWaitEvent(op->comm_stream, op->ev_bnd, 0));
+  FK_TRY(fk::exchange_post(op, y, op->comm_stream));
+  FK_CUDA(cudaEventRecord(op->ev_xchg, op->comm_stream));
+  FK_TRY(launch_range(op, x, y, nxy, op->nel - 2 * nxy, op->stream));
+  FK_CUDA(cudaStreamWaitEvent(op->stream, op->ev_xchg, 0));
+  return fk::exchange_finish(op, y, op->stream);
+}
+
 int apply_full(fk_op* op, const double* x, double* y, cudaStream_t s_override = nullptr) {
   cudaStream_t saved = op->stream;
   if (s_override) op->stream = s_override;
-  int rc = launch_local(op, x, y);
-  if (rc == FK_OK && op->comm) rc = fk::exchange_interface(op, y, op->stream);
+  int rc = FK_OK;
+  if (op->comm && op->comm->nranks > 1 && op->desc.nz_local >= 3) {
+    rc = apply_overlapped(op, x, y);
+  } else {
+    rc = launch_local(op, x, y);
+    if (rc == FK_OK && op->comm) rc = fk::exchange_interface(op, y, op->stream);
+  }
   if (rc == FK_OK && op->desc.dirichlet && op->n_ess > 0) {
     fk::ess_copy_kernel<<<grid_for(op->n_ess, 256, op->num_sms), 256, 0, op->stream>>>(
         y, x, op->ess, op->n_ess);
@@ -408,6 +447,9 @@ int fk_op_destroy(fk_op* op) {
   cudaFree(op->counter);
   cudaFree(op->hist);
   cudaFree(op->halo);
+  if (op->comm_stream) cudaStreamDestroy(op->comm_stream);
+  if (op->ev_bnd) cudaEventDestroy(op->ev_bnd);
+  if (op->ev_xchg) cudaEventDestroy(op->ev_xchg);
   if (op->ev0) cudaEventDestroy(op->ev0);
   if (op->ev1) cudaEventDestroy(op->ev1);
   if (op->ev2) cudaEventDestroy(op->ev2);
@@ -536,16 +578,8 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
     x_done = x_hi;
     FK_CUDA(cudaEventRecord(op->chunk_ev[2 * c], op->h2d));
     FK_CUDA(cudaStreamWaitEvent(op->stream, op->chunk_ev[2 * c], 0));
-    fk::OpView v = view(op);
-    const int64_t e0 = (int64_t)z0 * nxy, ne = (int64_t)(z1 - z0) * nxy;
-    v.gids += e0 * op->gs;
-    v.pa += e0 * op->ps;
-    v.nel = (int)ne;
-    const int64_t nb = (ne + op->kern->E - 1) / op->kern->E;
-    const int blocks = (int)std::max<int64_t>(
-        1, op->kern->persist ? std::min<int64_t>(nb, op->max_blocks) : nb);
-    op->kern->launch(v, op->stage_x, op->stage_y, blocks, op->stream);
-    FK_CUDA(cudaGetLastError());
+    FK_TRY(launch_range(op, op->stage_x, op->stage_y, (int64_t)z0 * nxy, (int64_t)(z1 - z0) * nxy,
+                        op->stream));
     FK_CUDA(cudaEventRecord(op->chunk_ev[2 * c + 1], op->stream));
     FK_CUDA(cudaStreamWaitEvent(op->d2h, op->chunk_ev[2 * c + 1], 0));
     const int64_t y_hi = (c == K - 1) ? op->npz_local : (int64_t)z1 * p;

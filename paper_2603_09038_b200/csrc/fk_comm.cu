@@ -102,7 +102,42 @@ int comm_setup(fk_op* op) {
   if (op->comm->nranks > 1 && op->halo == nullptr) {
     if (cudaMalloc(&op->halo, sizeof(double) * 2 * op->npx * op->npy) != cudaSuccess)
       return fk_set_error(FK_ENOMEM, "halo buffers");
+    if (cudaStreamCreateWithFlags(&op->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&op->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&op->ev_xchg, cudaEventDisableTiming) != cudaSuccess)
+      return fk_set_error(FK_ECUDA, "comm stream/events");
   }
+  return FK_OK;
+}
+
+int exchange_post(fk_op* op, double* y, cudaStream_t s) {
+  fk_comm* c = op->comm;
+  if (c == nullptr || c->nranks <= 1) return FK_OK;
+  NcclApi& api = nccl();
+  ncclComm_t comm = static_cast<ncclComm_t>(c->nccl);
+  const int64_t P = op->npx * op->npy;
+  NCCL_TRY(api.GroupStart());
+  if (c->rank > 0) {
+    NCCL_TRY(api.Send(y, P, ncclDouble, c->rank - 1, comm, s));
+    NCCL_TRY(api.Recv(op->halo, P, ncclDouble, c->rank - 1, comm, s));
+  }
+  if (c->rank < c->nranks - 1) {
+    NCCL_TRY(api.Send(y + op->ndof - P, P, ncclDouble, c->rank + 1, comm, s));
+    NCCL_TRY(api.Recv(op->halo + P, P, ncclDouble, c->rank + 1, comm, s));
+  }
+  NCCL_TRY(api.GroupEnd());
+  return FK_OK;
+}
+
+int exchange_finish(fk_op* op, double* y, cudaStream_t s) {
+  fk_comm* c = op->comm;
+  if (c == nullptr || c->nranks <= 1) return FK_OK;
+  const int64_t P = op->npx * op->npy;
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>((P + threads - 1) / threads, 4 * op->num_sms);
+  if (c->rank > 0) add_plane_kernel<<<blocks, threads, 0, s>>>(y, op->halo, P);
+  if (c->rank < c->nranks - 1) add_plane_kernel<<<blocks, threads, 0, s>>>(y + op->ndof - P, op->halo + P, P);
+  if (cudaGetLastError() != cudaSuccess) return fk_set_error(FK_ECUDA, "add_plane_kernel launch");
   return FK_OK;
 }
 

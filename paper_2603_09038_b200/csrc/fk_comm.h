@@ -17,6 +17,11 @@ int64_t owned_begin(const fk_op* op);
 int comm_setup(fk_op* op);
 // y_plane += neighbour's partial sum of the same plane, for both interfaces.
 int exchange_interface(fk_op* op, double* y, cudaStream_t s);
+// Split form for overlap: post the grouped send/recv of both interface planes
+// on stream s (after the boundary-layer elements), then add the received
+// partial sums on stream s2 (after the interior elements and a join).
+int exchange_post(fk_op* op, double* y, cudaStream_t s);
+int exchange_finish(fk_op* op, double* y, cudaStream_t s2);
 int allreduce_scalar(fk_op* op, double* dev_scalar, cudaStream_t s);
 
 }  // namespace fk

@@ -91,5 +91,7 @@ struct fk_op {
   // multi-rank
   fk_comm* comm = nullptr;
   double* halo = nullptr;  // receive buffers (2 planes)
+  cudaStream_t comm_stream = nullptr;           // NCCL plane exchange (overlaps interior elements)
+  cudaEvent_t ev_bnd = nullptr, ev_xchg = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
 };
