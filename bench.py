@@ -445,8 +445,8 @@ def run_sweep(a, peak):
             op = PAOperator(build_mesh(n, n, n), p, kind=kind)
             x = torch.randn(op.num_dofs, dtype=torch.float64, device="cuda")
             y = torch.empty_like(x)
-            for variant, cfg in ([("dfma", c) for c in range(6)] + [("dmma", c) for c in range(4)]
-                                 + [("eo", c) for c in range(4)]):
+            for variant, cfg in ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(4)]
+                                 + [("eo", c) for c in range(9)]):
                 try:
                     op.set_config(variant, cfg)
                 except NotImplementedError:

@@ -69,6 +69,7 @@ struct DfmaBody {
   using G = GlobalLayout<D, Q, NC>;
   using Tab = RowTables<D, Q>;
   static constexpr int LS = L::LS, LQ = L::LQ, P0 = L::P0, P1 = L::P1, Q3 = L::Q3;
+  static constexpr bool IP = false;  // W written to the T1/W region (not in place)
   static constexpr int XS = D * D * LS;
   static constexpr int DP = Tab::DP, QP = Tab::QP;
   static constexpr int E = E_, T = T_, EXTRA = 0;

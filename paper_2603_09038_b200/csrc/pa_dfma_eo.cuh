@@ -108,14 +108,24 @@ __device__ __forceinline__ void contract_eo(const double* __restrict__ t, const 
   }
 }
 
-template <int D, int Q, int NC, int E_, int T_>
+// IP (in place): stage C reads its T2 line into registers, the CTA syncs,
+// and W overwrites T2 in region 0; R then lives in region 1.  The two work
+// regions shrink from max(T2,R)+max(T1,W) to max(T2,W)+max(T1,R) doubles
+// per element, which buys one more resident CTA per SM at p=4.
+template <int D, int Q, int NC, int E_, int T_, bool IP_ = false>
 struct DfmaEoBody {
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
   using Tab = FoldTables<D, Q>;
-  static constexpr int LS = L::LS, LQ = L::LQ, P0 = L::P0, P1 = L::P1, Q3 = L::Q3;
+  static constexpr bool IP = IP_;
+  static constexpr int LS = L::LS, LQ = L::LQ, Q3 = L::Q3;
+  static constexpr int P0 = IP ? odd_up(cmax3(L::X_SZ, L::T2_SZ, L::W_SZ)) : L::P0;
+  static constexpr int P1 = IP ? odd_up(cmax(L::T1_SZ, L::R_SZ)) : L::P1;
+  static constexpr int WST = IP ? P0 : P1;  // element stride of the region holding W
+  static constexpr int RST = IP ? P1 : P0;  // ... and R
   static constexpr int XS = D * D * LS;
   static constexpr int E = E_, T = T_, EXTRA = 0;
+  static_assert(!IP || E * Q * Q <= T, "in-place stage C needs one pass over its lines");
 
   static void fill(Tab& tb, const double* B, const double* Gr) {
     double Bt[Q * D], Gt[Q * D];
@@ -190,26 +200,33 @@ struct DfmaEoBody {
     });
   }
 
-  // T2 [s][b][a][k] (line r = a + Q b) + D -> W [s][k][a][b]
+  // T2 [s][b][a][k] (line r = a + Q b) + D -> W [s][k][a][b] (region sw, stride WST)
   __device__ __forceinline__ static void stage_c(const Tab& tb, int it, const double* s0,
-                                                 const double* db, double* s1, int ne, double*) {
+                                                 const double* db, double* sw, int ne, double*) {
     const double* tab = tb.t[it & 1];
-    lines_loop<T, E * Q * Q>(ne * Q * Q, [&](int t) {
+    const int n = ne * Q * Q;
+    constexpr int NIT = (E * Q * Q + T - 1) / T;
+#pragma unroll
+    for (int pass = 0; pass < NIT; ++pass) {
+      const int t0 = threadIdx.x + pass * T;
+      const bool act = t0 < n;
+      const int t = act ? t0 : 0;
       const int e = t / (Q * Q), r = t - e * (Q * Q);
       const double* in = s0 + e * P0 + r * LS;
+      double tin[NC][D];
+#pragma unroll
+      for (int s = 0; s < NC; ++s)
+#pragma unroll
+        for (int k = 0; k < D; ++k) tin[s][k] = in[s * Q * Q * LS + k];
+      if constexpr (IP) __syncthreads();  // every T2 line is in registers: W may overwrite it
+      if (!act) continue;
       const double* pe = db + e * G::PS + r;
-      double* o = s1 + e * P1 + (r % Q) * LQ + (r / Q);
+      double* o = sw + e * WST + (r % Q) * LQ + (r / Q);
       if constexpr (NC == 3) {
-        double tz[D], g0[Q], g1[Q], g2[Q];
-#pragma unroll
-        for (int k = 0; k < D; ++k) tz[k] = in[k];
-        contract_eo<D, Q, +1>(tab + Tab::TB, tz, g0);
-#pragma unroll
-        for (int k = 0; k < D; ++k) tz[k] = in[Q * Q * LS + k];
-        contract_eo<D, Q, +1>(tab + Tab::TB, tz, g1);
-#pragma unroll
-        for (int k = 0; k < D; ++k) tz[k] = in[2 * Q * Q * LS + k];
-        contract_eo<D, Q, -1>(tab + Tab::TG, tz, g2);
+        double g0[Q], g1[Q], g2[Q];
+        contract_eo<D, Q, +1>(tab + Tab::TB, tin[0], g0);
+        contract_eo<D, Q, +1>(tab + Tab::TB, tin[1], g1);
+        contract_eo<D, Q, -1>(tab + Tab::TG, tin[NC - 1], g2);
 #pragma unroll
         for (int c = 0; c < Q; ++c) {
           const double* pc = pe + c * Q * Q;
@@ -231,27 +248,25 @@ struct DfmaEoBody {
 #pragma unroll
         for (int k = 0; k < D; ++k) o[2 * D * Q * LQ + k * Q * LQ] = w[k];
       } else {
-        double tz[D], g[Q], w[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) tz[k] = in[k];
-        contract_eo<D, Q, +1>(tab + Tab::TB, tz, g);
+        double g[Q], w[D];
+        contract_eo<D, Q, +1>(tab + Tab::TB, tin[0], g);
 #pragma unroll
         for (int c = 0; c < Q; ++c) g[c] *= pe[c * Q * Q];
         contract_eo<Q, D, +1>(tab + Tab::TBT, g, w);
 #pragma unroll
         for (int k = 0; k < D; ++k) o[k * Q * LQ] = w[k];
       }
-    });
+    }
   }
 
-  // W [s][k][a][b] (line u = a + Q k) -> R [s][k][j][a]
-  __device__ __forceinline__ static void stage_d(const Tab& tb, int it, const double* s1, double* s0,
+  // W [s][k][a][b] (line u = a + Q k) -> R [s][k][j][a]   (W stride WST, R stride RST)
+  __device__ __forceinline__ static void stage_d(const Tab& tb, int it, const double* sw, double* sr,
                                                  int ne, double*) {
     const double* tab = tb.t[it & 1];
     lines_loop<T, E * Q * D>(ne * Q * D, [&](int t) {
       const int e = t / (Q * D), u = t - e * (Q * D);
-      const double* in = s1 + e * P1 + u * LQ;
-      double* o = s0 + e * P0 + (u / Q) * D * LQ + (u % Q);
+      const double* in = sw + e * WST + u * LQ;
+      double* o = sr + e * RST + (u / Q) * D * LQ + (u % Q);
       double wv[Q], r0[D];
 #pragma unroll
       for (int b = 0; b < Q; ++b) wv[b] = in[b];
@@ -273,12 +288,12 @@ struct DfmaEoBody {
   }
 
   // R [s][k][j][a] (line v = j + D k) -> y (atomic scatter-add)
-  __device__ __forceinline__ static void stage_e(const Tab& tb, int it, const double* s0,
+  __device__ __forceinline__ static void stage_e(const Tab& tb, int it, const double* sr,
                                                  const int* gslot, double* y, int ne, double*) {
     const double* tab = tb.t[it & 1];
     lines_loop<T, E * D * D>(ne * D * D, [&](int t) {
       const int e = t / (D * D), v = t - e * (D * D);
-      const double* in = s0 + e * P0 + v * LQ;
+      const double* in = sr + e * RST + v * LQ;
       const int* g = gslot + e * G::GS + v * D;
       double rv[Q], out[D];
 #pragma unroll

@@ -112,6 +112,7 @@ struct DmmaBody {
   using Tab = Tables<D, Q>;
   static constexpr int E = E_, T = T_, NW = T_ / 32;
   static constexpr int LS = L::LS, LQ = L::LQ, P0 = L::P0, P1 = L::P1, Q3 = L::Q3, D3 = L::D3;
+  static constexpr bool IP = false;
   static constexpr int XS = D * D * LS;
   static constexpr int KD = cdiv(D, 4), KQ = cdiv(Q, 4), K2Q = cdiv(2 * Q, 4);
   static constexpr int NQ = cdiv(Q, 8), N2Q = cdiv(2 * Q, 8), ND = cdiv(D, 8);

@@ -30,7 +30,7 @@ void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaSt
   typename Body::Tab tb;
   Body::fill(tb, v.B, v.G);
   pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG>
-      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body::E, Body::EXTRA, DG>::BYTES, s>>>(
+      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body, DG>::BYTES, s>>>(
           tb, x, y, v.gids, v.pa, v.ebits, v.nel);
 }
 
@@ -53,7 +53,7 @@ KernelEntry entry(int variant, int cfg) {
   k.E = Body::E;
   k.T = Body::T;
   k.persist = PERSIST;
-  k.smem = PipeSmem<D, Q, NC, Body::E, Body::EXTRA, DG>::BYTES;
+  k.smem = PipeSmem<D, Q, NC, Body, DG>::BYTES;
   k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG>);
   k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG>;
   k.diag = &launch_diag<D, Q, NC>;
@@ -85,6 +85,19 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, O1, true>(FK_VARIANT_EO, 1));
   out.push_back(entry<D, Q, NC, O2, true, true>(FK_VARIANT_EO, 2));
   out.push_back(entry<D, Q, NC, O1, true, true>(FK_VARIANT_EO, 3));
+  using O1i = DfmaEoBody<D, Q, NC, E1, round32(E1 * Q * Q), true>;
+  using O2i = DfmaEoBody<D, Q, NC, E2, round32(E2 * Q * Q), true>;
+  out.push_back(entry<D, Q, NC, O2i, true>(FK_VARIANT_EO, 4));        // W over T2 (smaller smem)
+  out.push_back(entry<D, Q, NC, O1i, true>(FK_VARIANT_EO, 5));
+  out.push_back(entry<D, Q, NC, O2i, true, true>(FK_VARIANT_EO, 6));
+  out.push_back(entry<D, Q, NC, O1i, true, true>(FK_VARIANT_EO, 7));
+  // large batches (E0 ~ 288/q^2 elements, one stage-C line per thread): the
+  // light BP1 element needs little smem, so more elements per CTA amortise
+  // the per-batch barriers and pipeline bookkeeping
+  using O0i = DfmaEoBody<D, Q, NC, E0, round32(E0 * Q * Q), true>;
+  using F0 = DfmaBody<D, Q, NC, E0, round32(E0 * Q * Q), 1>;
+  out.push_back(entry<D, Q, NC, O0i, true>(FK_VARIANT_EO, 8));
+  out.push_back(entry<D, Q, NC, F0, true>(FK_VARIANT_DFMA, 6));
 }
 
 }  // namespace

@@ -24,10 +24,11 @@
 
 namespace fk {
 
-template <int D, int Q, int NC, int E, int EXTRA, bool DG = false>
+template <int D, int Q, int NC, class Body, bool DG = false>
 struct PipeSmem {
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
+  static constexpr int E = Body::E, EXTRA = Body::EXTRA;
   static constexpr int XS = D * D * L::LS;  // X buffer doubles per element
   static constexpr int NG = 3;              // gather-id slots (batches b, b+1, b+2)
   // byte offsets (16-byte aligned where bulk copies land)
@@ -36,8 +37,8 @@ struct PipeSmem {
   static constexpr size_t OFF_GS = OFF_DB + (DG ? 0ull : 8ull * E * G::PS);  // NG gid slots
   static constexpr size_t OFF_MS = OFF_GS + 4ull * NG * E * G::GS;     // NG bit slots
   static constexpr size_t OFF_S0 = OFF_MS + 4ull * NG * E * G::MS;
-  static constexpr size_t OFF_S1 = OFF_S0 + 8ull * E * L::P0;
-  static constexpr size_t OFF_XB = OFF_S1 + 8ull * E * L::P1;         // 2 X buffers
+  static constexpr size_t OFF_S1 = OFF_S0 + 8ull * E * Body::P0;
+  static constexpr size_t OFF_XB = OFF_S1 + 8ull * E * Body::P1;      // 2 X buffers
   static constexpr size_t OFF_EX = (OFF_XB + 8ull * 2 * E * XS + 15) / 16 * 16;
   static constexpr size_t BYTES = OFF_EX + 8ull * EXTRA;
 };
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   constexpr int E = Body::E, T = Body::T;
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
-  using S = PipeSmem<D, Q, NC, E, Body::EXTRA, DG>;
+  using S = PipeSmem<D, Q, NC, Body, DG>;
   constexpr int D3 = L::D3, LS = L::LS, XS = S::XS, NG = S::NG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar_d = reinterpret_cast<uint64_t*>(smem_raw + S::OFF_BAR);
@@ -68,6 +69,9 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   double* s1 = reinterpret_cast<double*>(smem_raw + S::OFF_S1);
   double* xb = reinterpret_cast<double*>(smem_raw + S::OFF_XB);
   double* ex = reinterpret_cast<double*>(smem_raw + S::OFF_EX);
+  // W (stage C -> D) and R (stage D -> E) regions: in-place bodies put W over T2
+  double* sw = Body::IP ? s0 : s1;
+  double* sr = Body::IP ? s1 : s0;
 
   const int nbatch = (nel + E - 1) / E;
   if ((int)blockIdx.x >= nbatch) return;
@@ -162,20 +166,20 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     Body::stage_b(tb, it, s1, s0, ne, ex);
     __syncthreads();
     if constexpr (DG) {
-      Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, s1, ne, ex);
+      Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex);
     } else {
       mbar_wait(bar_d, ph_d);
       ph_d ^= 1u;
-      Body::stage_c(tb, it, s0, db, s1, ne, ex);
+      Body::stage_c(tb, it, s0, db, sw, ne, ex);
     }
     __syncthreads();
     if (nb < nbatch && threadIdx.x == 0) {
       fence_proxy_async();
       issue_d(nb);
     }
-    Body::stage_d(tb, it, s1, s0, ne, ex);
+    Body::stage_d(tb, it, sw, sr, ne, ex);
     __syncthreads();
-    Body::stage_e(tb, it, s0, gs + gslot * E * G::GS, y, ne, ex);
+    Body::stage_e(tb, it, sr, gs + gslot * E * G::GS, y, ne, ex);
     __syncthreads();
   };
 

@@ -117,8 +117,8 @@ def test_apply_matches_oracle_all_orders(variant, kind, p, qoff):
     assert normwise(y, P.apply(x)) <= PARITY_TOL
 
 
-LAUNCH_CONFIGS = ([("dfma", c) for c in range(6)] + [("dmma", c) for c in range(4)]
-                  + [("eo", c) for c in range(4)])
+LAUNCH_CONFIGS = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(4)]
+                  + [("eo", c) for c in range(9)])
 
 
 @pytest.mark.parametrize("variant,cfg", LAUNCH_CONFIGS)
