@@ -80,12 +80,12 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // profiles/r01_sweep_v5_noloop_pingpong.jsonl).  DFMA wins at every order on
 // sm_100a: DMMA and DFMA share the 37 TFLOP/s FP64 pipe, and DMMA's 8x8x4
 // padding wastes 14-88% of it at these shapes.
-// (variant, cfg) per order, best of profiles/r01_sweep_v8_inplace.jsonl
+// (variant, cfg) per order, best of profiles/r01_sweep_v9.jsonl
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
-const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, D_, O_, O_};
-const int kAutoCfg3[9] = {0, 1, 5, 1, 4, 4, 2, 3, 7};
-const int kAutoVar1[9] = {D_, D_, O_, D_, O_, O_, O_, O_, O_};
-const int kAutoCfg1[9] = {0, 3, 5, 1, 5, 1, 4, 0, 1};
+const int kAutoVar3[9] = {D_, D_, O_, O_, O_, O_, D_, O_, O_};
+const int kAutoCfg3[9] = {0, 6, 5, 1, 0, 4, 2, 2, 6};
+const int kAutoVar1[9] = {D_, D_, O_, D_, D_, O_, O_, O_, O_};
+const int kAutoCfg1[9] = {0, 6, 8, 6, 6, 8, 5, 0, 1};
 
 int auto_variant(int nc, int p, int q) {
   (void)q;

@@ -180,7 +180,9 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     Body::stage_d(tb, it, sw, sr, ne, ex);
     __syncthreads();
     Body::stage_e(tb, it, sr, gs + gslot * E * G::GS, y, ne, ex);
-    __syncthreads();
+    // no barrier here: every thread passes the barrier after the next batch's
+    // finish_x only after its own stage E, and nothing before that barrier
+    // touches the regions stage E reads (R, this batch's gid slot)
   };
 
   if constexpr (PERSIST) {
