@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="elements per direction (per-rank slab is n^3)")
     ap.add_argument("--variant", default="auto", choices=["auto", "dfma", "dmma", "eo"])
     ap.add_argument("--sweep", default=None, help="also run the p=1..8 DFMA/DMMA sweep, JSON lines to FILE")
+    ap.add_argument("--sweep-cfgs", default=None,
+                    help="restrict the sweep to these geometries, e.g. 'eo0,eo9,dfma2'")
+    ap.add_argument("--sweep-kinds", default="diffusion,mass")
+    ap.add_argument("--sweep-orders", default="1,2,3,4,5,6,7,8")
     ap.add_argument("--cg", default=None, choices=["weak", "strong"],
                     help="run the 100-iteration Jacobi-PCG benchmark (BASELINE configs[3]/[4])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -439,14 +443,18 @@ def run_sweep(a, peak):
     from paper_2603_09038_b200 import PAOperator, build_mesh
 
     out = []
-    for kind in ("diffusion", "mass"):
-        for p in range(1, 9):
+    cfgs = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(3)]
+            + [("eo", c) for c in range(9)])
+    if a.sweep_cfgs:
+        want = set(a.sweep_cfgs.split(","))
+        cfgs = [vc for vc in cfgs if f"{vc[0]}{vc[1]}" in want]
+    for kind in a.sweep_kinds.split(","):
+        for p in [int(v) for v in a.sweep_orders.split(",")]:
             n = SWEEP_N[p]
             op = PAOperator(build_mesh(n, n, n), p, kind=kind)
             x = torch.randn(op.num_dofs, dtype=torch.float64, device="cuda")
             y = torch.empty_like(x)
-            for variant, cfg in ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(4)]
-                                 + [("eo", c) for c in range(9)]):
+            for variant, cfg in cfgs:
                 try:
                     op.set_config(variant, cfg)
                 except NotImplementedError:

@@ -168,8 +168,9 @@ int select_kernel(fk_op* op, int variant) {
     if (occ < 1) return fail(FK_EUNSUPPORTED, "fused kernel does not fit on an SM (smem %zu)", k->smem);
     const int64_t nbatch = (op->nel + k->E - 1) / k->E;
     op->max_blocks = occ * op->num_sms;
+    if (op->block_cap > 0) op->max_blocks = std::min(op->max_blocks, op->block_cap);
     op->blocks = k->persist
-                     ? (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ * op->num_sms))
+                     ? (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)op->max_blocks))
                      : (int)std::max<int64_t>(1, nbatch);
   }
   return FK_OK;
@@ -375,6 +376,9 @@ int fk_op_setup(fk_op* op) {
   op->gs = fk::gid_stride(op->d);
   op->ms = fk::bits_stride(op->d);
   if (const char* c = std::getenv("FK_CFG")) op->cfg = std::atoi(c);
+  // test hook: cap the persistent grid so small meshes run several batches per
+  // CTA (exercises the cross-batch prefetch pipeline of pa_pipe.cuh)
+  if (const char* c = std::getenv("FK_MAX_BLOCKS")) op->block_cap = std::max(1, std::atoi(c));
   if (op->gids == nullptr) FK_CUDA(cudaMalloc(&op->gids, sizeof(int) * (op->nel * op->gs + 16)));
   if (op->host_gids.empty()) {
     fk::restriction_kernel<<<grid_for(op->nel * op->gs, 256, op->num_sms), 256, 0, s>>>(

@@ -81,6 +81,7 @@ struct fk_op {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t chunk_ev[32] = {};
   int max_blocks = 0;  // resident CTAs of the fused kernel on the device
+  int block_cap = 0;   // FK_MAX_BLOCKS test hook (0: none)
   // CG / reduction workspace
   double* work = nullptr;  // r, z, p, Ap, dinv (5 * ndof)
   double* scal = nullptr;  // scalars

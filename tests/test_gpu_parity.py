@@ -117,7 +117,7 @@ def test_apply_matches_oracle_all_orders(variant, kind, p, qoff):
     assert normwise(y, P.apply(x)) <= PARITY_TOL
 
 
-LAUNCH_CONFIGS = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(4)]
+LAUNCH_CONFIGS = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(3)]
                   + [("eo", c) for c in range(9)])
 
 
@@ -136,6 +136,31 @@ def test_every_launch_config(variant, cfg, kind, p):
             op.set_config(variant, cfg)
         except NotImplementedError as ex:  # geometry exceeds 227 KB smem at this order
             pytest.skip(str(ex))
+        y = op.apply(dev(x)).cpu().numpy()
+        ref = P.constrained_apply(x, P.boundary()) if dirichlet else P.apply(x)
+        assert normwise(y, ref) <= PARITY_TOL, (op.launch, dirichlet)
+
+
+@pytest.mark.parametrize("variant,cfg", LAUNCH_CONFIGS)
+@pytest.mark.parametrize("kind", ["mass", "diffusion"])
+@pytest.mark.parametrize("p", range(1, 9))
+def test_every_launch_config_multi_batch(variant, cfg, kind, p, monkeypatch):
+    """Persistent grid capped at 3 CTAs (FK_MAX_BLOCKS test hook): every CTA
+    walks several batches, so the cross-batch prefetches (x gather one batch
+    ahead, gather-id slots two ahead, PA data to smem / L2 / registers) and the
+    ping-pong buffers are exercised, with a ragged last batch."""
+    monkeypatch.setenv("FK_MAX_BLOCKS", "3")
+    n = (5, 4, 3) if p <= 4 else (3, 3, 3)
+    P = bp.Problem(kind, *n, p)
+    x = np.random.default_rng(p + 7).standard_normal(P.ndof)
+    for dirichlet in (False, True):
+        op = make(kind, n, p, dirichlet=dirichlet)
+        try:
+            op.set_config(variant, cfg)
+        except NotImplementedError as ex:
+            pytest.skip(str(ex))
+        if (variant, cfg) != ("dfma", 5):  # dfma5: one batch per CTA, no persistent grid
+            assert op.launch[2] <= 3
         y = op.apply(dev(x)).cpu().numpy()
         ref = P.constrained_apply(x, P.boundary()) if dirichlet else P.apply(x)
         assert normwise(y, ref) <= PARITY_TOL, (op.launch, dirichlet)
