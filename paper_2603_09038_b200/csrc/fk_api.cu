@@ -76,16 +76,17 @@ int grid_for(int64_t n, int threads, int num_sms) {
 }
 
 // Per-order automatic choice (FK_VARIANT_AUTO): variant and launch geometry
-// with the highest measured GDOF/s in the p-sweep on B200 (DESIGN.md §4.4,
-// profiles/r01_sweep_v5_noloop_pingpong.jsonl).  DFMA wins at every order on
-// sm_100a: DMMA and DFMA share the 37 TFLOP/s FP64 pipe, and DMMA's 8x8x4
-// padding wastes 14-88% of it at these shapes.
-// (variant, cfg) per order, best of profiles/r01_sweep_v9.jsonl
+// with the highest measured GDOF/s in the p-sweep on B200.
+// The FP64-FMA line kernels win at every order on sm_100a: DMMA and DFMA share
+// the 37 TFLOP/s FP64 pipe, and DMMA's 8x8x4 padding wastes 14-88% of it at
+// these shapes.
+// (variant, cfg) per order, best of profiles/r01_sweep_v11_static_tables.jsonl
+// (tools/auto_table.py)
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
-const int kAutoVar3[9] = {D_, D_, O_, O_, O_, O_, D_, O_, O_};
-const int kAutoCfg3[9] = {0, 6, 5, 1, 0, 4, 2, 2, 6};
-const int kAutoVar1[9] = {D_, D_, O_, D_, D_, O_, O_, O_, O_};
-const int kAutoCfg1[9] = {0, 6, 8, 6, 6, 8, 5, 0, 1};
+const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
+const int kAutoCfg3[9] = {0, 14, 1, 11, 1, 1, 14, 18, 10};
+const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
+const int kAutoCfg1[9] = {0, 9, 6, 9, 2, 18, 10, 14, 14};
 
 int auto_variant(int nc, int p, int q) {
   (void)q;
@@ -149,7 +150,7 @@ int select_kernel(fk_op* op, int variant) {
                     k->smem, max_smem);
       // default geometry too large: first compiled geometry that fits
       const fk::KernelEntry* alt = nullptr;
-      for (int c = 0; c < 8 && alt == nullptr; ++c) {
+      for (int c = 0; c < 32 && alt == nullptr; ++c) {
         const fk::KernelEntry* t = fk::find_kernel_cfg(op->nc, op->d, op->q, v, c);
         if (t && t->smem <= (size_t)max_smem) alt = t;
       }
@@ -764,28 +765,40 @@ int fk_op_time_apply(fk_op* op, const double* x, double* y, int reps, const void
   if (op == nullptr || x == nullptr || y == nullptr || reps < 1) return fail(FK_EINVAL, "bad argument");
   if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
   DeviceGuard g(op->device);
-  double tot_a = 0.0, tot_k = 0.0;
-  for (int r = 0; r < reps; ++r) {
+  // all reps enqueued back to back (no host sync in between), so the events
+  // see steady-state launches, not the host's launch latency after an idle GPU
+  std::vector<cudaEvent_t> ev(4 * (size_t)reps);
+  for (auto& e : ev) FK_CUDA(cudaEventCreate(&e));
+  int rc = FK_OK;
+  for (int r = 0; r < reps && rc == FK_OK; ++r) {
+    cudaEvent_t* e = ev.data() + 4 * r;
     if (flush && flush_bytes)
       FK_CUDA(cudaMemsetAsync(const_cast<void*>(flush), r & 0xff, flush_bytes, op->stream));
-    FK_CUDA(cudaEventRecord(op->ev0, op->stream));
+    FK_CUDA(cudaEventRecord(e[0], op->stream));
     FK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * op->ndof, op->stream));
-    FK_CUDA(cudaEventRecord(op->ev1, op->stream));
+    FK_CUDA(cudaEventRecord(e[1], op->stream));
     op->kern->launch(view(op), x, y, op->blocks, op->stream);
     FK_CUDA(cudaGetLastError());
-    FK_CUDA(cudaEventRecord(op->ev2, op->stream));
-    if (op->comm) FK_TRY(fk::exchange_interface(op, y, op->stream));
+    FK_CUDA(cudaEventRecord(e[2], op->stream));
+    if (op->comm) rc = fk::exchange_interface(op, y, op->stream);
     if (op->desc.dirichlet && op->n_ess > 0)
       fk::ess_copy_kernel<<<grid_for(op->n_ess, 256, op->num_sms), 256, 0, op->stream>>>(
           y, x, op->ess, op->n_ess);
-    FK_CUDA(cudaEventRecord(op->ev3, op->stream));
-    FK_CUDA(cudaEventSynchronize(op->ev3));
-    float a = 0.f, k = 0.f;
-    FK_CUDA(cudaEventElapsedTime(&a, op->ev0, op->ev3));
-    FK_CUDA(cudaEventElapsedTime(&k, op->ev1, op->ev2));
-    tot_a += a;
-    tot_k += k;
+    FK_CUDA(cudaEventRecord(e[3], op->stream));
   }
+  double tot_a = 0.0, tot_k = 0.0;
+  if (rc == FK_OK) {
+    FK_CUDA(cudaEventSynchronize(ev[4 * (size_t)reps - 1]));
+    for (int r = 0; r < reps; ++r) {
+      float a = 0.f, k = 0.f;
+      FK_CUDA(cudaEventElapsedTime(&a, ev[4 * r], ev[4 * r + 3]));
+      FK_CUDA(cudaEventElapsedTime(&k, ev[4 * r + 1], ev[4 * r + 2]));
+      tot_a += a;
+      tot_k += k;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc != FK_OK) return rc;
   if (ms_apply) *ms_apply = tot_a / reps;
   if (ms_kernel) *ms_kernel = tot_k / reps;
   return FK_OK;

@@ -35,7 +35,14 @@ struct OpView {
 };
 
 // Host mirror of GlobalLayout (pa_common.cuh): padded per-element strides.
-inline int64_t pa_stride(int npa, int q) { return ((int64_t)npa * q * q * q + 1) / 2 * 2; }
+// PA element stride: even (16-byte bulk-copy granules) and = q^2 (+1) mod 16,
+// so the stage-C lines of consecutive elements of a batch (q^2 per element)
+// continue the bank sequence instead of colliding (tools/smem_strides.py)
+inline int64_t pa_stride(int npa, int q) {
+  int64_t n = ((int64_t)npa * q * q * q + 1) / 2 * 2;
+  while (((n - q * q) % 16 + 16) % 16 > 1) n += 2;
+  return n;
+}
 inline int64_t gid_stride(int d) { return ((int64_t)d * d * d + 3) / 4 * 4; }
 inline int64_t bits_stride(int d) { return (((int64_t)d * d * d + 31) / 32 + 3) / 4 * 4; }
 

@@ -60,13 +60,16 @@ struct LineLayout {
   }
 };
 
+// PA element stride: even and = q^2 (+1) mod 16 (see fk_internal.h pa_stride)
+constexpr int pa_pad(int n, int q) { return (((n - q * q) % 16 + 16) % 16 > 1) ? pa_pad(n + 2, q) : n; }
+
 // Global (HBM) layout strides per element, padded so every per-batch range
 // is a 16-byte multiple (cp.async.bulk granularity).  Host code mirrors
 // these in fk_api.cu (pa_stride / gid_stride / bits_stride).
 template <int D, int Q, int NC>
 struct GlobalLayout {
   static constexpr int NPA = (NC == 3) ? 6 : 1;
-  static constexpr int PS = ((NPA * Q * Q * Q + 1) / 2) * 2;  // doubles of PA data per element
+  static constexpr int PS = pa_pad(((NPA * Q * Q * Q + 1) / 2) * 2, Q);  // doubles of PA data per element
   static constexpr int GS = ((D * D * D + 3) / 4) * 4;        // int32 gather ids per element
   static constexpr int MW = (D * D * D + 31) / 32;            // Dirichlet bit words per element
   static constexpr int MS = ((MW + 3) / 4) * 4;               // padded

@@ -108,23 +108,111 @@ __device__ __forceinline__ void contract_eo(const double* __restrict__ t, const 
   }
 }
 
-// IP (in place): stage C reads its T2 line into registers, the CTA syncs,
-// and W overwrites T2 in region 0; R then lives in region 1.  The two work
-// regions shrink from max(T2,R)+max(T1,W) to max(T2,W)+max(T1,R) doubles
-// per element, which buys one more resident CTA per SM at p=4.
-template <int D, int Q, int NC, int E_, int T_, bool IP_ = false>
+// ---------------------------------------------------------------------------
+// Shared-memory layouts.  Every intermediate buffer has a padded linear layout
+//     word(e, s, i1, i2, i3) = e*SE + s*SS + i1*S1 + i2*S2 + i3*S3
+// in the canonical index order
+//     X  (i, j, k)   gathered dofs            T1 (a, j, k)   after x
+//     T2 (a, b, k)   after y                  W  (a, b, k)   after z, D, z^T
+//     R  (a, j, k)   after y^T
+// and every stage maps its threads to lines through a LineMap (element-major
+// or element-minor, either line index fastest).  The layouts and maps of the
+// tuned geometries come from tools/smem_strides.py, which minimises
+// shared-memory wavefronts (bank conflicts and partially filled half-warps)
+// for the stage access patterns below.
+template <int SE, int SS, int S1, int S2, int S3>
+struct BufLay {
+  static constexpr int se = SE;
+  __device__ __forceinline__ static int at(int e, int s, int i1, int i2, int i3) {
+    return e * SE + s * SS + i1 * S1 + i2 * S2 + i3 * S3;
+  }
+};
+
+// thread t -> (element e, line indices p1 < N1, p2 < N2)
+//   M = 0: element-major, p1 fastest     M = 1: element-major, p2 fastest
+//   M = 2: element-minor, p1 fastest     M = 3: element-minor, p2 fastest
+template <int M, int E, int N1, int N2>
+__device__ __forceinline__ void line_map(int t, int& e, int& p1, int& p2) {
+  constexpr int L = N1 * N2;
+  int l;
+  if constexpr (M < 2) {
+    e = t / L;
+    l = t - e * L;
+  } else {
+    l = t / E;
+    e = t - l * E;
+  }
+  if constexpr (M == 0 || M == 2) {
+    p2 = l / N1;
+    p1 = l - p2 * N1;
+  } else {
+    p1 = l / N2;
+    p2 = l - p1 * N2;
+  }
+}
+
+// The line layout of the first even-odd kernels (odd line pitches LS = D|1,
+// LQ = Q|1; W over T1 or, in place, over T2), expressed as BufLays.
+template <int D, int Q, int NC, bool IP>
+struct EoLayDefault {
+  using L = LineLayout<D, Q, NC>;
+  static constexpr int LS = L::LS, LQ = L::LQ;
+  static constexpr int P0 = IP ? odd_up(cmax3(L::X_SZ, L::T2_SZ, L::W_SZ)) : L::P0;
+  static constexpr int P1 = IP ? odd_up(cmax(L::T1_SZ, L::R_SZ)) : L::P1;
+  static constexpr int WST = IP ? P0 : P1, RST = IP ? P1 : P0;
+  static constexpr bool W_OVER_T2 = IP;
+  static constexpr int MG = 0, MA = 0, MB = 1, MC = 0, MD = 0, ME = 0;
+  using X = BufLay<D * D * LS, 0, 1, LS, D * LS>;
+  using T1 = BufLay<P1, Q * D * LS, D * LS, 1, LS>;
+  using T2 = BufLay<P0, Q * Q * LS, LS, Q * LS, 1>;
+  using W = BufLay<WST, D * Q * LQ, LQ, 1, Q * LQ>;
+  using R = BufLay<RST, D * D * LQ, 1, LQ, D * LQ>;
+};
+
+// Even-odd FP64-FMA body over layout policy LP (EoLayDefault or a searched
+// layout).  W_OVER_T2 (in place): stage C reads its T2 line into registers,
+// the CTA syncs, and W overwrites T2 in region 0; R then lives in region 1 —
+// max(T2,W)+max(T1,R) instead of max(T2,R)+max(T1,W) doubles per element.
+//
+// PP (ping-pong tables, pa_dfma.cuh header): batch `it` reads table copy it&1,
+// so the loads stay loop-variant and ptxas cannot hoist the whole table into
+// (spilled) registers.  At p >= 6 with three components the dynamic index
+// instead makes ptxas fall back from uniform LDCU to per-thread LDC and holds
+// 126-165 registers (vs 75-88 static); PP = false uses the static copy 0.
+template <int D, int Q, int NC, int E_, int T_, class LP, bool PP = true>
 struct DfmaEoBody {
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
   using Tab = FoldTables<D, Q>;
-  static constexpr bool IP = IP_;
-  static constexpr int LS = L::LS, LQ = L::LQ, Q3 = L::Q3;
-  static constexpr int P0 = IP ? odd_up(cmax3(L::X_SZ, L::T2_SZ, L::W_SZ)) : L::P0;
-  static constexpr int P1 = IP ? odd_up(cmax(L::T1_SZ, L::R_SZ)) : L::P1;
-  static constexpr int WST = IP ? P0 : P1;  // element stride of the region holding W
-  static constexpr int RST = IP ? P1 : P0;  // ... and R
-  static constexpr int XS = D * D * LS;
+  using LX = typename LP::X;
+  using LT1 = typename LP::T1;
+  using LT2 = typename LP::T2;
+  using LW = typename LP::W;
+  using LR = typename LP::R;
+  static constexpr bool IP = LP::W_OVER_T2;
+  static constexpr int Q3 = L::Q3;
   static constexpr int E = E_, T = T_, EXTRA = 0;
+  // region 0: T2 then R (or W); region 1: T1 then W (or R); per-element
+  // strides as the pipeline expects (it allocates E * P0 and E * P1 doubles)
+  static constexpr int R0 = cmax(E * LT2::se, E * (IP ? LW::se : LR::se));
+  static constexpr int R1 = cmax(E * LT1::se, E * (IP ? LR::se : LW::se));
+  static constexpr int P0 = (R0 + E - 1) / E, P1 = (R1 + E - 1) / E;
+  // X buffer (pa_pipe.cuh gathers into it through xoff / gather_map)
+  static constexpr bool XLAY = true;
+  static constexpr int XS = LX::se;
+  __device__ __forceinline__ static int xoff(int e, int l) {
+    const int k = l / (D * D), j = (l / D) % D, i = l % D;
+    return LX::at(e, 0, i, j, k);
+  }
+  __device__ __forceinline__ static void gather_map(int t, int& e, int& l) {
+    if constexpr (LP::MG < 2) {
+      e = t / (D * D * D);
+      l = t - e * (D * D * D);
+    } else {
+      l = t / E;
+      e = t - l * E;
+    }
+  }
   static_assert(!IP || E * Q * Q <= T, "in-place stage C needs one pass over its lines");
 
   static void fill(Tab& tb, const double* B, const double* Gr) {
@@ -144,84 +232,92 @@ struct DfmaEoBody {
 
   __device__ static void init(const Tab&, double*) {}
 
-  // X [v=(j,k)][i] -> T1 [s][a][k][j]
+  // run f(e, p1, p2) over the stage's lines of the batch's ne elements
+  template <int M, int N1, int N2, typename F>
+  __device__ __forceinline__ static void lines(int ne, F f) {
+    constexpr int N = E * N1 * N2;
+    auto one = [&](int t) {
+      int e, p1, p2;
+      line_map<M, E, N1, N2>(t, e, p1, p2);
+      if (e < ne) f(e, p1, p2);
+    };
+    if constexpr (N <= T) {
+      if ((int)threadIdx.x < N) one((int)threadIdx.x);
+    } else {
+      for (int t = threadIdx.x; t < N; t += T) one(t);
+    }
+  }
+
+  // X (i, j, k) -> T1 (a, j, k): thread per line (j, k)
   __device__ __forceinline__ static void stage_a(const Tab& tb, int it, const double* xb, double* s1,
                                                  int ne, double*) {
-    const double* tab = tb.t[it & 1];
-    lines_loop<T, E * D * D>(ne * D * D, [&](int t) {
-      const int e = t / (D * D), v = t - e * (D * D);
-      const double* in = xb + e * XS + v * LS;
+    const double* tab = tb.t[PP ? (it & 1) : 0];
+    lines<LP::MA, D, D>(ne, [&](int e, int j, int k) {
       double xr[D], bx[Q];
 #pragma unroll
-      for (int i = 0; i < D; ++i) xr[i] = in[i];
-      double* o = s1 + e * P1 + (v / D) * LS + (v % D);
+      for (int i = 0; i < D; ++i) xr[i] = xb[LX::at(e, 0, i, j, k)];
       contract_eo<D, Q, +1>(tab + Tab::TB, xr, bx);
 #pragma unroll
-      for (int a = 0; a < Q; ++a) o[a * D * LS] = bx[a];
+      for (int a = 0; a < Q; ++a) s1[LT1::at(e, 0, a, j, k)] = bx[a];
       if constexpr (NC == 3) {
         double gx[Q];
         contract_eo<D, Q, -1>(tab + Tab::TG, xr, gx);
 #pragma unroll
-        for (int a = 0; a < Q; ++a) o[Q * D * LS + a * D * LS] = gx[a];
+        for (int a = 0; a < Q; ++a) s1[LT1::at(e, 1, a, j, k)] = gx[a];
       }
     });
   }
 
-  // T1 [s][a][k][j] (line u = k + D a) -> T2 [s][b][a][k]
+  // T1 (a, j, k) -> T2 (a, b, k): thread per line (a, k)
   __device__ __forceinline__ static void stage_b(const Tab& tb, int it, const double* s1, double* s0,
                                                  int ne, double*) {
-    const double* tab = tb.t[it & 1];
-    lines_loop<T, E * D * Q>(ne * D * Q, [&](int t) {
-      const int e = t / (D * Q), u = t - e * (D * Q);
-      const double* in = s1 + e * P1 + u * LS;
-      double bx[D];
+    const double* tab = tb.t[PP ? (it & 1) : 0];
+    lines<LP::MB, Q, D>(ne, [&](int e, int a, int k) {
+      double bx[D], c[Q];
 #pragma unroll
-      for (int j = 0; j < D; ++j) bx[j] = in[j];
-      double* o = s0 + e * P0 + (u / D) * LS + (u % D);
-      double c[Q];
+      for (int j = 0; j < D; ++j) bx[j] = s1[LT1::at(e, 0, a, j, k)];
       if constexpr (NC == 3) {
         double gx[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) gx[j] = in[Q * D * LS + j];
+        for (int j = 0; j < D; ++j) gx[j] = s1[LT1::at(e, 1, a, j, k)];
         contract_eo<D, Q, +1>(tab + Tab::TB, gx, c);  // comp0 = B_y G_x
 #pragma unroll
-        for (int b = 0; b < Q; ++b) o[b * Q * LS] = c[b];
+        for (int b = 0; b < Q; ++b) s0[LT2::at(e, 0, a, b, k)] = c[b];
         contract_eo<D, Q, -1>(tab + Tab::TG, bx, c);  // comp1 = G_y B_x
 #pragma unroll
-        for (int b = 0; b < Q; ++b) o[Q * Q * LS + b * Q * LS] = c[b];
+        for (int b = 0; b < Q; ++b) s0[LT2::at(e, 1, a, b, k)] = c[b];
         contract_eo<D, Q, +1>(tab + Tab::TB, bx, c);  // comp2 = B_y B_x
 #pragma unroll
-        for (int b = 0; b < Q; ++b) o[2 * Q * Q * LS + b * Q * LS] = c[b];
+        for (int b = 0; b < Q; ++b) s0[LT2::at(e, 2, a, b, k)] = c[b];
       } else {
         contract_eo<D, Q, +1>(tab + Tab::TB, bx, c);
 #pragma unroll
-        for (int b = 0; b < Q; ++b) o[b * Q * LS] = c[b];
+        for (int b = 0; b < Q; ++b) s0[LT2::at(e, 0, a, b, k)] = c[b];
       }
     });
   }
 
-  // T2 [s][b][a][k] (line r = a + Q b) + D -> W [s][k][a][b] (region sw, stride WST)
+  // T2 (a, b, k) + D -> W (a, b, k): thread per line (a, b); W region sw
   __device__ __forceinline__ static void stage_c(const Tab& tb, int it, const double* s0,
                                                  const double* db, double* sw, int ne, double*) {
-    const double* tab = tb.t[it & 1];
-    const int n = ne * Q * Q;
-    constexpr int NIT = (E * Q * Q + T - 1) / T;
+    const double* tab = tb.t[PP ? (it & 1) : 0];
+    constexpr int N = E * Q * Q;
+    constexpr int NIT = (N + T - 1) / T;
 #pragma unroll
     for (int pass = 0; pass < NIT; ++pass) {
       const int t0 = threadIdx.x + pass * T;
-      const bool act = t0 < n;
-      const int t = act ? t0 : 0;
-      const int e = t / (Q * Q), r = t - e * (Q * Q);
-      const double* in = s0 + e * P0 + r * LS;
+      int e, a, b;
+      line_map<LP::MC, E, Q, Q>(t0 < N ? t0 : 0, e, a, b);
+      const bool act = t0 < N && e < ne;
+      if (!act) e = 0;
       double tin[NC][D];
 #pragma unroll
       for (int s = 0; s < NC; ++s)
 #pragma unroll
-        for (int k = 0; k < D; ++k) tin[s][k] = in[s * Q * Q * LS + k];
+        for (int k = 0; k < D; ++k) tin[s][k] = s0[LT2::at(e, s, a, b, k)];
       if constexpr (IP) __syncthreads();  // every T2 line is in registers: W may overwrite it
       if (!act) continue;
-      const double* pe = db + e * G::PS + r;
-      double* o = sw + e * WST + (r % Q) * LQ + (r / Q);
+      const double* pe = db + e * G::PS + a + Q * b;
       if constexpr (NC == 3) {
         double g0[Q], g1[Q], g2[Q];
         contract_eo<D, Q, +1>(tab + Tab::TB, tin[0], g0);
@@ -240,13 +336,13 @@ struct DfmaEoBody {
         double w[D];
         contract_eo<Q, D, +1>(tab + Tab::TBT, g0, w);
 #pragma unroll
-        for (int k = 0; k < D; ++k) o[k * Q * LQ] = w[k];
+        for (int k = 0; k < D; ++k) sw[LW::at(e, 0, a, b, k)] = w[k];
         contract_eo<Q, D, +1>(tab + Tab::TBT, g1, w);
 #pragma unroll
-        for (int k = 0; k < D; ++k) o[D * Q * LQ + k * Q * LQ] = w[k];
+        for (int k = 0; k < D; ++k) sw[LW::at(e, 1, a, b, k)] = w[k];
         contract_eo<Q, D, -1>(tab + Tab::TGT, g2, w);
 #pragma unroll
-        for (int k = 0; k < D; ++k) o[2 * D * Q * LQ + k * Q * LQ] = w[k];
+        for (int k = 0; k < D; ++k) sw[LW::at(e, 2, a, b, k)] = w[k];
       } else {
         double g[Q], w[D];
         contract_eo<D, Q, +1>(tab + Tab::TB, tin[0], g);
@@ -254,55 +350,50 @@ struct DfmaEoBody {
         for (int c = 0; c < Q; ++c) g[c] *= pe[c * Q * Q];
         contract_eo<Q, D, +1>(tab + Tab::TBT, g, w);
 #pragma unroll
-        for (int k = 0; k < D; ++k) o[k * Q * LQ] = w[k];
+        for (int k = 0; k < D; ++k) sw[LW::at(e, 0, a, b, k)] = w[k];
       }
     }
   }
 
-  // W [s][k][a][b] (line u = a + Q k) -> R [s][k][j][a]   (W stride WST, R stride RST)
+  // W (a, b, k) -> R (a, j, k): thread per line (a, k)
   __device__ __forceinline__ static void stage_d(const Tab& tb, int it, const double* sw, double* sr,
                                                  int ne, double*) {
-    const double* tab = tb.t[it & 1];
-    lines_loop<T, E * Q * D>(ne * Q * D, [&](int t) {
-      const int e = t / (Q * D), u = t - e * (Q * D);
-      const double* in = sw + e * WST + u * LQ;
-      double* o = sr + e * RST + (u / Q) * D * LQ + (u % Q);
+    const double* tab = tb.t[PP ? (it & 1) : 0];
+    lines<LP::MD, Q, D>(ne, [&](int e, int a, int k) {
       double wv[Q], r0[D];
 #pragma unroll
-      for (int b = 0; b < Q; ++b) wv[b] = in[b];
+      for (int b = 0; b < Q; ++b) wv[b] = sw[LW::at(e, 0, a, b, k)];
       contract_eo<Q, D, +1>(tab + Tab::TBT, wv, r0);  // rG = B^T w0 (BP1: r = B^T w)
 #pragma unroll
-      for (int j = 0; j < D; ++j) o[j * LQ] = r0[j];
+      for (int j = 0; j < D; ++j) sr[LR::at(e, 0, a, j, k)] = r0[j];
       if constexpr (NC == 3) {
         double r1[D];
 #pragma unroll
-        for (int b = 0; b < Q; ++b) wv[b] = in[D * Q * LQ + b];
+        for (int b = 0; b < Q; ++b) wv[b] = sw[LW::at(e, 1, a, b, k)];
         contract_eo<Q, D, -1>(tab + Tab::TGT, wv, r0);  // G^T w1
 #pragma unroll
-        for (int b = 0; b < Q; ++b) wv[b] = in[2 * D * Q * LQ + b];
+        for (int b = 0; b < Q; ++b) wv[b] = sw[LW::at(e, 2, a, b, k)];
         contract_eo<Q, D, +1>(tab + Tab::TBT, wv, r1);  // B^T w2
 #pragma unroll
-        for (int j = 0; j < D; ++j) o[D * D * LQ + j * LQ] = r0[j] + r1[j];
+        for (int j = 0; j < D; ++j) sr[LR::at(e, 1, a, j, k)] = r0[j] + r1[j];
       }
     });
   }
 
-  // R [s][k][j][a] (line v = j + D k) -> y (atomic scatter-add)
+  // R (a, j, k) -> y (atomic scatter-add): thread per line (j, k)
   __device__ __forceinline__ static void stage_e(const Tab& tb, int it, const double* sr,
                                                  const int* gslot, double* y, int ne, double*) {
-    const double* tab = tb.t[it & 1];
-    lines_loop<T, E * D * D>(ne * D * D, [&](int t) {
-      const int e = t / (D * D), v = t - e * (D * D);
-      const double* in = sr + e * RST + v * LQ;
-      const int* g = gslot + e * G::GS + v * D;
+    const double* tab = tb.t[PP ? (it & 1) : 0];
+    lines<LP::ME, D, D>(ne, [&](int e, int j, int k) {
+      const int* g = gslot + e * G::GS + D * (j + D * k);
       double rv[Q], out[D];
 #pragma unroll
-      for (int a = 0; a < Q; ++a) rv[a] = in[a];
+      for (int a = 0; a < Q; ++a) rv[a] = sr[LR::at(e, 0, a, j, k)];
       if constexpr (NC == 3) {
         double o2[D];
         contract_eo<Q, D, -1>(tab + Tab::TGT, rv, out);  // G^T rG
 #pragma unroll
-        for (int a = 0; a < Q; ++a) rv[a] = in[D * D * LQ + a];
+        for (int a = 0; a < Q; ++a) rv[a] = sr[LR::at(e, 1, a, j, k)];
         contract_eo<Q, D, +1>(tab + Tab::TBT, rv, o2);  // B^T rB
 #pragma unroll
         for (int i = 0; i < D; ++i) atomicAdd(y + g[i], out[i] + o2[i]);

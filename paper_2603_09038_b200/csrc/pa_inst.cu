@@ -11,6 +11,7 @@
 #include "pa_diag.cuh"
 #include "pa_dfma.cuh"
 #include "pa_dfma_eo.cuh"
+#include "pa_eo_layouts.cuh"
 #include "pa_dmma.cuh"
 #include "pa_pipe.cuh"
 
@@ -60,6 +61,27 @@ KernelEntry entry(int variant, int cfg) {
   return k;
 }
 
+template <int D, int Q, int NC, int E, bool IP, bool PP>
+using TunedEo = DfmaEoBody<D, Q, NC, E, round32(E * Q * Q), EoLayTuned<D, Q, NC, E, round32(E * Q * Q), IP>, PP>;
+
+// nine tuned even-odd geometries from cfg c0: (E2, E1) x (smem D, D via L2) x
+// (W over T1, W over T2), then E0 in place
+template <int D, int Q, int NC, bool PP>
+void add_tuned_eo(std::vector<KernelEntry>& out, int c0) {
+  constexpr int E0 = base_E(Q);
+  constexpr int E1 = E0 / 2 > 0 ? E0 / 2 : 1;
+  constexpr int E2 = E0 / 4 > 0 ? E0 / 4 : 1;
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, PP>, true>(FK_VARIANT_EO, c0 + 0));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, PP>, true>(FK_VARIANT_EO, c0 + 1));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, PP>, true, true>(FK_VARIANT_EO, c0 + 2));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, PP>, true, true>(FK_VARIANT_EO, c0 + 3));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, PP>, true>(FK_VARIANT_EO, c0 + 4));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, true, PP>, true>(FK_VARIANT_EO, c0 + 5));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, PP>, true, true>(FK_VARIANT_EO, c0 + 6));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, true, PP>, true, true>(FK_VARIANT_EO, c0 + 7));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, PP>, true>(FK_VARIANT_EO, c0 + 8));
+}
+
 // Compiled launch geometries (cfg index per variant; cfg 0 is the default).
 // Measured per order in the sweep (profiles/r01_sweep_*).
 template <int D, int Q, int NC>
@@ -79,25 +101,16 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true>(FK_VARIANT_DMMA, 0));
   out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E0, 256>, true>(FK_VARIANT_DMMA, 1));
   out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true, true>(FK_VARIANT_DMMA, 2));
-  using O1 = DfmaEoBody<D, Q, NC, E1, round32(E1 * Q * Q)>;
-  using O2 = DfmaEoBody<D, Q, NC, E2, round32(E2 * Q * Q)>;
-  out.push_back(entry<D, Q, NC, O2, true>(FK_VARIANT_EO, 0));
-  out.push_back(entry<D, Q, NC, O1, true>(FK_VARIANT_EO, 1));
-  out.push_back(entry<D, Q, NC, O2, true, true>(FK_VARIANT_EO, 2));
-  out.push_back(entry<D, Q, NC, O1, true, true>(FK_VARIANT_EO, 3));
-  using O1i = DfmaEoBody<D, Q, NC, E1, round32(E1 * Q * Q), true>;
-  using O2i = DfmaEoBody<D, Q, NC, E2, round32(E2 * Q * Q), true>;
-  out.push_back(entry<D, Q, NC, O2i, true>(FK_VARIANT_EO, 4));        // W over T2 (smaller smem)
-  out.push_back(entry<D, Q, NC, O1i, true>(FK_VARIANT_EO, 5));
-  out.push_back(entry<D, Q, NC, O2i, true, true>(FK_VARIANT_EO, 6));
-  out.push_back(entry<D, Q, NC, O1i, true, true>(FK_VARIANT_EO, 7));
-  // large batches (E0 ~ 288/q^2 elements, one stage-C line per thread): the
-  // light BP1 element needs little smem, so more elements per CTA amortise
-  // the per-batch barriers and pipeline bookkeeping
-  using O0i = DfmaEoBody<D, Q, NC, E0, round32(E0 * Q * Q), true>;
   using F0 = DfmaBody<D, Q, NC, E0, round32(E0 * Q * Q), 1>;
-  out.push_back(entry<D, Q, NC, O0i, true>(FK_VARIANT_EO, 8));
   out.push_back(entry<D, Q, NC, F0, true>(FK_VARIANT_DFMA, 6));
+  // even-odd bodies.  cfg 0: the line layout of the first EO kernels (reference
+  // point); cfgs 1-9: smem layouts searched by tools/smem_strides.py
+  // (pa_eo_layouts.cuh) with ping-pong tables; cfgs 10-18: the same with a
+  // static table copy (see DfmaEoBody PP).
+  using O2 = DfmaEoBody<D, Q, NC, E2, round32(E2 * Q * Q), EoLayDefault<D, Q, NC, false>>;
+  out.push_back(entry<D, Q, NC, O2, true>(FK_VARIANT_EO, 0));
+  add_tuned_eo<D, Q, NC, true>(out, 1);
+  add_tuned_eo<D, Q, NC, false>(out, 10);
 }
 
 }  // namespace

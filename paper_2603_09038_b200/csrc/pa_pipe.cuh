@@ -19,17 +19,44 @@
 // contractions feklab/tensor.py:177-283, PA data feklab/operator.py:132-193.
 #pragma once
 
+#include <type_traits>
+
 #include "pa_async.cuh"
 #include "pa_common.cuh"
 
 namespace fk {
+
+// X buffer addressing: bodies with their own layout (XLAY, pa_dfma_eo.cuh)
+// provide xoff(e, l) / gather_map(t, e, l); the others use the line layout
+// X[e][j + D k][i] with pitch LS and an element-major gather.
+template <class B, class = void>
+struct HasXLay : std::false_type {};
+template <class B>
+struct HasXLay<B, std::void_t<decltype(B::XLAY)>> : std::true_type {};
+
+template <int D, int Q, int NC, class Body, bool XL = HasXLay<Body>::value>
+struct XAddr {
+  using L = LineLayout<D, Q, NC>;
+  static constexpr int XS = D * D * L::LS;
+  __device__ __forceinline__ static int off(int e, int l) { return e * XS + (l / D) * L::LS + (l % D); }
+  __device__ __forceinline__ static void map(int t, int& e, int& l) {
+    e = t / L::D3;
+    l = t - e * L::D3;
+  }
+};
+template <int D, int Q, int NC, class Body>
+struct XAddr<D, Q, NC, Body, true> {
+  static constexpr int XS = Body::XS;
+  __device__ __forceinline__ static int off(int e, int l) { return Body::xoff(e, l); }
+  __device__ __forceinline__ static void map(int t, int& e, int& l) { Body::gather_map(t, e, l); }
+};
 
 template <int D, int Q, int NC, class Body, bool DG = false>
 struct PipeSmem {
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
   static constexpr int E = Body::E, EXTRA = Body::EXTRA;
-  static constexpr int XS = D * D * L::LS;  // X buffer doubles per element
+  static constexpr int XS = XAddr<D, Q, NC, Body>::XS;  // X buffer doubles per element
   static constexpr int NG = 3;              // gather-id slots (batches b, b+1, b+2)
   // byte offsets (16-byte aligned where bulk copies land)
   static constexpr size_t OFF_BAR = 0;                                 // 4 mbarriers
@@ -58,7 +85,8 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
   using S = PipeSmem<D, Q, NC, Body, DG>;
-  constexpr int D3 = L::D3, LS = L::LS, XS = S::XS, NG = S::NG;
+  using XA = XAddr<D, Q, NC, Body>;
+  constexpr int D3 = L::D3, XS = S::XS, NG = S::NG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar_d = reinterpret_cast<uint64_t*>(smem_raw + S::OFF_BAR);
   uint64_t* bar_g = bar_d + 1;  // [NG]
@@ -111,8 +139,9 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     const int e0 = b * E, ne = min(E, nel - e0);
     const int* g = gs + gslot * E * G::GS;
     for (int t = threadIdx.x; t < E * D3; t += T) {
-      const int e = t / D3, l = t - e * D3;
-      double* dst = xdst + e * XS + (l / D) * LS + (l % D);
+      int e, l;
+      XA::map(t, e, l);
+      double* dst = xdst + XA::off(e, l);
       if (e < ne) cp_async8(dst, x + g[e * G::GS + l]);
       else *dst = 0.0;
     }
@@ -122,9 +151,12 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     cp_async_wait_all();
     if (dirichlet) {
       const uint32_t* m = ms + gslot * E * G::MS;
-      for (int t = threadIdx.x; t < ne * D3; t += T) {
-        const int e = t / D3, l = t - e * D3;
-        if ((m[e * G::MS + (l >> 5)] >> (l & 31)) & 1u) xsrc[e * XS + (l / D) * LS + (l % D)] = 0.0;
+      // same thread -> (e, l) map as issue_x: cp.async.wait_group only covers
+      // this thread's own copies
+      for (int t = threadIdx.x; t < E * D3; t += T) {
+        int e, l;
+        XA::map(t, e, l);
+        if (e < ne && ((m[e * G::MS + (l >> 5)] >> (l & 31)) & 1u)) xsrc[XA::off(e, l)] = 0.0;
       }
     }
   };
