@@ -603,7 +603,7 @@ int fk_op_diagonal(fk_op* op, double* diag) {
   FK_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * op->ndof, op->stream));
   const fk::KernelEntry* k = fk::find_kernel(op->nc, op->d, op->q, FK_VARIANT_DFMA);
   if (k == nullptr || k->diag == nullptr) return fail(FK_EUNSUPPORTED, "no diagonal kernel");
-  k->diag(view(op), diag, op->nel, grid_for(op->nel * op->d * op->d * op->d, 128, op->num_sms),
+  k->diag(view(op), diag, op->nel, (int)std::min<int64_t>(op->nel, (int64_t)op->num_sms * 16),
           op->stream);
   FK_CUDA(cudaGetLastError());
   if (op->comm) FK_TRY(fk::exchange_interface(op, diag, op->stream));
