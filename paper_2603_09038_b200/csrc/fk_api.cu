@@ -568,7 +568,8 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
     FK_CUDA(cudaStreamCreateWithFlags(&op->d2h, cudaStreamNonBlocking));
     for (auto& e : op->chunk_ev) FK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  const int K = std::min(nzl, 8);
+  int K = std::min(nzl, 8);
+  if (const char* c = std::getenv("FK_HOST_CHUNKS")) K = std::max(1, std::min({nzl, std::atoi(c), 15}));
   const int64_t P = op->npx * op->npy, nxy = (int64_t)op->desc.nx * op->desc.ny;
   const int p = op->p;
   FK_CUDA(cudaEventRecord(op->chunk_ev[30], op->stream));  // order after prior work
