@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--sweep-orders", default="1,2,3,4,5,6,7,8")
     ap.add_argument("--cg", default=None, choices=["weak", "strong"],
                     help="run the 100-iteration Jacobi-PCG benchmark (BASELINE configs[3]/[4])")
+    ap.add_argument("--mixed", action="store_true",
+                    help="acoustic-gravity FusedPA block apply (paper Table VII: H1 p=4 x L2 p=3, "
+                         "q=5, ~540 M dofs; SURVEY.md §8f) + an RK4 step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -436,6 +439,70 @@ def run_cg(a):
         dist.destroy_process_group()
 
 
+def run_mixed(a):
+    """FusedPA apply of the acoustic-gravity block operator on 1 GPU at the
+    paper's Table VII configuration (H1 p=4 / L2 p=3, q=5, 128^3 elements =
+    537.7 M dofs; PAPER.md:647-664 reports 46.60 GDOF/s for DMMA Fused PA on
+    GB200).  Inputs resident in HBM (dmat 18.9 GB > L2); GDOF/s = state dofs /
+    apply time.  Also times one device RK4 step (4 applies + axpys)."""
+    import torch
+
+    from paper_2603_09038_b200 import MixedOperator, MixedState, build_mesh
+
+    torch.cuda.set_device(0)
+    p = a.p or 4
+    n = a.n or 128
+    op = MixedOperator(build_mesh(n, n, n), p, p - 1, p + 1)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    s = MixedState(torch.randn(op.u_shape, dtype=torch.float64, device="cuda", generator=g),
+                   torch.randn(op.num_p, dtype=torch.float64, device="cuda", generator=g))
+    out = op.zero_state(device=True)
+    sampler = ClockSampler(0)
+    with sampler:
+        for _ in range(max(3, a.warmup)):
+            op.apply(s, out=out)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(a.steps):
+            op.apply(s, out=out)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / a.steps
+        _, ms_kernel = op.time_apply(s, out, min(a.steps, 50))
+        op.rk4(s, 1e-6, 1)
+        torch.cuda.synchronize()
+        ev0.record()
+        op.rk4(s, 1e-6, 2)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms_rk4 = ev0.elapsed_time(ev1) / 2
+    peak, peak_src = measured_peaks()
+    alg = op.bytes_per_apply
+    published = 46.60
+    value = op.num_dofs / (ms * 1e-3) / 1e9
+    print(json.dumps({
+        "metric": "GDOF/s of the FusedPA acoustic-gravity block apply (H1 p=4 x L2 p=3, q=5)",
+        "value": value, "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_published_gb200_dmma_fused_pa": value / published, "dtype": "f64",
+        "data": "synthetic (u, p ~ N(0,1)), unit-cube Cartesian hex mesh",
+        "config": {"workload": f"BlockOperator FusedPA apply {n}^3 elements, order_p={p}, "
+                               f"order_u={p - 1}, q={p + 1} ({op.num_dofs} dofs: "
+                               f"{op.num_dofs - op.num_p} velocity + {op.num_p} pressure)",
+                   "launch": {"elems_per_block": op.launch[0], "threads": op.launch[1],
+                              "blocks": op.launch[2]},
+                   "l2": "inputs larger than L2 (dmat 9 comps/point, ~19 GB)"},
+        "roofline": {"bound": "hbm", "achieved": alg / (ms_kernel * 1e-3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": alg / (ms_kernel * 1e-3) / 1e9 / peak,
+                     "peak_source": peak_src, "kernel_ms": ms_kernel,
+                     "algorithmic_bytes_per_launch": alg},
+        "rk4_step_ms": ms_rk4, "rk4_gdofs_per_apply": 4 * op.num_dofs / (ms_rk4 * 1e-3) / 1e9,
+        "clocks": sampler.summary(),
+    }), flush=True)
+    op.close()
+
+
 def run_sweep(a, peak):
     """p=1..8 BP3/BP1 sweep, DFMA vs DMMA, written as JSON lines to a file."""
     import torch
@@ -484,6 +551,8 @@ def main():
         run_reference(a)
     elif a.cg:
         run_cg(a)
+    elif a.mixed:
+        run_mixed(a)
     else:
         run_ours(a)
 

@@ -148,6 +148,67 @@ int fk_op_time_apply(fk_op* op, const double* x_dev, double* y_dev, int reps,
                      const void* flush_dev, size_t flush_bytes,
                      double* ms_apply, double* ms_kernel);
 
+
+/* ---------------------------------------------------------------------------
+ * Acoustic-gravity block operator (feklab/operator.py BlockOperator,
+ * strategy FusedPA).  State [u; p]: u = 3 velocity
+ * components in the discontinuous space of order_u, element blocks
+ * (3, nel, (order_u+1)^3) as State.u (operator.py:63-90); p = pressure dofs
+ * of the continuous H1 space of order_p (h1_restriction numbering).
+ *   out_u =  cs * B_u^T D^T grad p            (_pressure_to_velocity, :288-301)
+ *   out_p = -cs * G^T grad^T D B_u u          (_velocity_to_pressure, :303-319)
+ * D = dmat = w|J| J^-1 (9 components per point, :137-144) is read once per
+ * element for both blocks.  Compiled spaces: order_u = order_p - 1,
+ * num_quad_1d = order_p + 1, order_p = 2..8 (the reference default 4/3/5).
+ * No absorbing faces or surface gravity (:400-440).
+ * ------------------------------------------------------------------------- */
+typedef struct fk_mix fk_mix;
+
+typedef struct fk_mix_desc {
+  int order_p, order_u, num_quad_1d;
+  int nx, ny, nz;              /* build_mesh(nx, ny, nz, extents) */
+  double jac_diag[3];          /* Mesh.jacobian_diag (mesh.py:56-60) */
+  double jac_det;              /* Mesh.jacobian_det */
+  const double* Bp;            /* host q x (order_p+1): pressure Basis1D.values */
+  const double* Gp;            /* host q x (order_p+1): pressure Basis1D.gradients */
+  const double* Bu;            /* host q x (order_u+1): velocity Basis1D.values */
+  const double* w;             /* host q: quad_weights */
+  const double* rho;           /* host per-element density (nel) or NULL -> rho_scalar */
+  const double* bulk;          /* host per-element bulk modulus or NULL -> bulk_scalar */
+  double rho_scalar, bulk_scalar;
+  double coupling_scale;       /* BlockOperator coupling_scale */
+  int device;
+  void* stream;                /* cudaStream_t */
+} fk_mix_desc;
+
+typedef struct fk_mix_info {
+  int64_t nel, ndof_p, ndof_u; /* ndof_u = 3 * nel * (order_u+1)^3 */
+  int64_t pa_bytes;
+  int elems_per_block, threads_per_block, blocks;
+  int64_t smem_bytes;
+} fk_mix_info;
+
+int fk_mix_create(fk_mix** out, const fk_mix_desc* desc);
+/* device E-restriction, dmat and the lumped mass diagonals (setup_quad_data) */
+int fk_mix_setup(fk_mix* m);
+int fk_mix_destroy(fk_mix* m);
+int fk_mix_get_info(const fk_mix* m, fk_mix_info* info);
+/* BlockOperator.apply: out_u overwritten, out_p overwritten (device pointers) */
+int fk_mix_apply(fk_mix* m, const double* u, const double* p, double* out_u, double* out_p);
+/* BlockOperator.apply_fused_normal: velocity -> assembled pressure -> velocity */
+int fk_mix_fused_normal(fk_mix* m, const double* u, double* out_u);
+/* BlockOperator.apply_mass_inverse: u = ru / lump_u, p = rp / lump_p */
+int fk_mix_mass_inverse(fk_mix* m, const double* ru, const double* rp, double* u, double* p);
+/* `steps` classical RK4 steps of [u,p]' = Minv(-A [u,p]) in place (rk4_step,
+ * operator.py:506-531, no forcing); four fused applies per step. */
+int fk_mix_rk4(fk_mix* m, double* u, double* p, double dt, int steps);
+/* parity hooks: lumped diagonals (device copies) and restriction rows (host int64) */
+int fk_mix_lumped(fk_mix* m, double* lump_u, double* lump_p);
+int fk_mix_restriction(fk_mix* m, int64_t* host_out);
+/* mean ms per apply (incl. the out_p memset) and of the fused kernel over reps */
+int fk_mix_time_apply(fk_mix* m, const double* u, const double* p, double* out_u, double* out_p,
+                      int reps, double* ms_apply, double* ms_kernel);
+
 #ifdef __cplusplus
 }
 #endif

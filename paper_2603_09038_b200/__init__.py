@@ -20,6 +20,8 @@ from .fem import (
     h1_node_coords,
     h1_restriction,
 )
+from .mixed import MixedOperator, rk4_step
+from .mixed import State as MixedState
 from .operator import (
     Comm,
     PAData,
@@ -33,7 +35,8 @@ from .operator import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "Basis1D", "Comm", "Counters", "GeometryError", "Mesh", "PAData", "PAOperator",
+    "Basis1D", "Comm", "Counters", "GeometryError", "Mesh", "MixedOperator", "MixedState",
+    "PAData", "PAOperator", "rk4_step",
     "Restriction", "ShapeError", "boundary_dofs", "build_mesh", "bytes_per_apply",
     "cg_solve", "flops_per_element", "gauss_points", "gll_points", "h1_gather_ids",
     "h1_node_coords", "h1_restriction", "setup_pa_data", "__version__",

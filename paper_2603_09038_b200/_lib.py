@@ -42,6 +42,9 @@ EXPORTS = (
     "fk_op_set_essential",
     "fk_cg_solve", "fk_dot", "fk_comm_unique_id", "fk_comm_create", "fk_comm_destroy",
     "fk_op_time_apply",
+    "fk_mix_create", "fk_mix_setup", "fk_mix_destroy", "fk_mix_get_info", "fk_mix_apply",
+    "fk_mix_fused_normal", "fk_mix_mass_inverse", "fk_mix_rk4", "fk_mix_lumped",
+    "fk_mix_restriction", "fk_mix_time_apply",
 )
 
 
@@ -80,6 +83,43 @@ class FkOpInfo(ctypes.Structure):
         ("elems_per_block", ctypes.c_int),
         ("threads_per_block", ctypes.c_int),
         ("blocks", ctypes.c_int),
+    ]
+
+
+class FkMixDesc(ctypes.Structure):
+    _fields_ = [
+        ("order_p", ctypes.c_int),
+        ("order_u", ctypes.c_int),
+        ("num_quad_1d", ctypes.c_int),
+        ("nx", ctypes.c_int),
+        ("ny", ctypes.c_int),
+        ("nz", ctypes.c_int),
+        ("jac_diag", ctypes.c_double * 3),
+        ("jac_det", ctypes.c_double),
+        ("Bp", ctypes.POINTER(ctypes.c_double)),
+        ("Gp", ctypes.POINTER(ctypes.c_double)),
+        ("Bu", ctypes.POINTER(ctypes.c_double)),
+        ("w", ctypes.POINTER(ctypes.c_double)),
+        ("rho", ctypes.POINTER(ctypes.c_double)),
+        ("bulk", ctypes.POINTER(ctypes.c_double)),
+        ("rho_scalar", ctypes.c_double),
+        ("bulk_scalar", ctypes.c_double),
+        ("coupling_scale", ctypes.c_double),
+        ("device", ctypes.c_int),
+        ("stream", ctypes.c_void_p),
+    ]
+
+
+class FkMixInfo(ctypes.Structure):
+    _fields_ = [
+        ("nel", ctypes.c_int64),
+        ("ndof_p", ctypes.c_int64),
+        ("ndof_u", ctypes.c_int64),
+        ("pa_bytes", ctypes.c_int64),
+        ("elems_per_block", ctypes.c_int),
+        ("threads_per_block", ctypes.c_int),
+        ("blocks", ctypes.c_int),
+        ("smem_bytes", ctypes.c_int64),
     ]
 
 
@@ -132,6 +172,17 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "fk_comm_create": (i, [ctypes.POINTER(vp), vp, i, i, i]),
         "fk_comm_destroy": (i, [vp]),
         "fk_op_time_apply": (i, [vp, vp, vp, i, vp, ctypes.c_size_t, pd, pd]),
+        "fk_mix_create": (i, [ctypes.POINTER(vp), ctypes.POINTER(FkMixDesc)]),
+        "fk_mix_setup": (i, [vp]),
+        "fk_mix_destroy": (i, [vp]),
+        "fk_mix_get_info": (i, [vp, ctypes.POINTER(FkMixInfo)]),
+        "fk_mix_apply": (i, [vp, vp, vp, vp, vp]),
+        "fk_mix_fused_normal": (i, [vp, vp, vp]),
+        "fk_mix_mass_inverse": (i, [vp, vp, vp, vp, vp]),
+        "fk_mix_rk4": (i, [vp, vp, vp, d, i]),
+        "fk_mix_lumped": (i, [vp, vp, vp]),
+        "fk_mix_restriction": (i, [vp, ctypes.POINTER(i64)]),
+        "fk_mix_time_apply": (i, [vp, vp, vp, vp, vp, i, pd, pd]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -14,6 +14,7 @@
 
 #include "fk_cg.cuh"
 #include "fk_comm.h"
+#include "fk_error.h"
 #include "fk_internal.h"
 #include "fk_setup.cuh"
 
@@ -23,7 +24,7 @@
 
 static thread_local std::string g_last_error;
 
-static int fail(int code, const char* fmt, ...) {
+int fk_fail(int code, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
   va_start(ap, fmt);
@@ -32,35 +33,11 @@ static int fail(int code, const char* fmt, ...) {
   g_last_error = buf;
   return code;
 }
-
-#define FK_CUDA(call)                                                                         \
-  do {                                                                                        \
-    cudaError_t e_ = (call);                                                                  \
-    if (e_ != cudaSuccess)                                                                    \
-      return fail(e_ == cudaErrorMemoryAllocation ? FK_ENOMEM : FK_ECUDA, "%s: %s (%s:%d)", \
-                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
-  } while (0)
-
-#define FK_TRY(call)         \
-  do {                       \
-    int rc_ = (call);        \
-    if (rc_ != FK_OK) return rc_; \
-  } while (0)
+#define fail fk_fail
 
 namespace {
 
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
+using DeviceGuard = FkDeviceGuard;
 
 std::vector<fk::KernelEntry>& registry() {
   static std::vector<fk::KernelEntry> reg;

@@ -1,0 +1,542 @@
+// fk_mixed.cu — C-ABI of the acoustic-gravity block operator (include/fk.h,
+// fk_mix_*): setup of the PA data and lumped mass diagonals, the fused
+// FusedPA apply (mix_pipe.cuh), the composed normal operator, the lumped mass
+// inverse and a device RK4 driver.  Reference: feklab/operator.py:105-193
+// (QuadData / setup_quad_data), :221-397 (BlockOperator), :506-531 (rk4_step).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "fk_error.h"
+#include "mix_pipe.cuh"
+
+namespace {
+
+using fk::MixArgs;
+
+// Compiled (order_p, order_u, q): the paper's H1(p) x L2(p-1) pairs with
+// q = p+1 (the reference default is p=4, u=3, q=5, operator.py:227-229).
+constexpr int kMixMaxP = 8;
+
+struct MixKernel {
+  int dp = 0, du = 0, q = 0, E = 0, T = 0, ps = 0, gs = 0;
+  size_t smem = 0;
+  const void* f_both = nullptr;
+  const void* f_tau = nullptr;
+  const void* f_vb = nullptr;
+  void (*launch)(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
+                 const MixArgs& a, int mode, int blocks, cudaStream_t s) = nullptr;
+};
+
+enum { MIX_BOTH = 0, MIX_TAU = 1, MIX_VB = 2 };
+
+constexpr int round32(int n) { return (n + 31) / 32 * 32; }
+
+template <int DP, int DU, int Q>
+struct MixGeom {
+  static constexpr int NA = DP * DP + 3 * DU * DU, NB = Q * DP + 3 * Q * DU, NC = 2 * Q * Q;
+  static constexpr int NMAX = NB > NA ? (NB > NC ? NB : NC) : (NA > NC ? NA : NC);
+  static constexpr int E = 192 / NMAX > 0 ? 192 / NMAX : 1;
+  static constexpr int T = round32(E * NMAX) > 384 ? 384 : round32(E * NMAX);
+};
+
+template <int DP, int DU, int Q>
+void mix_launch(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
+                const MixArgs& a, int mode, int blocks, cudaStream_t s) {
+  using G = MixGeom<DP, DU, Q>;
+  fk::MixTables<DP, DU, Q> tb;
+  tb.fill(Bp, Gp, Bu);
+  const size_t smem = fk::MixSmem<DP, DU, Q, G::E>::BYTES;
+  if (mode == MIX_BOTH)
+    fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true><<<blocks, G::T, smem, s>>>(tb, a);
+  else if (mode == MIX_TAU)
+    fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false><<<blocks, G::T, smem, s>>>(tb, a);
+  else
+    fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true><<<blocks, G::T, smem, s>>>(tb, a);
+}
+
+template <int P>
+MixKernel mix_entry() {
+  constexpr int DP = P + 1, DU = P, Q = P + 1;
+  using G = MixGeom<DP, DU, Q>;
+  using L = fk::MixLayout<DP, DU, Q>;
+  MixKernel k;
+  k.dp = DP;
+  k.du = DU;
+  k.q = Q;
+  k.E = G::E;
+  k.T = G::T;
+  k.ps = L::PS;
+  k.gs = L::GS;
+  k.smem = fk::MixSmem<DP, DU, Q, G::E>::BYTES;
+  k.f_both = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true>);
+  k.f_tau = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false>);
+  k.f_vb = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true>);
+  k.launch = &mix_launch<DP, DU, Q>;
+  return k;
+}
+
+const std::vector<MixKernel>& mix_registry() {
+  static const std::vector<MixKernel> reg = {mix_entry<2>(), mix_entry<3>(), mix_entry<4>(),
+                                             mix_entry<5>(), mix_entry<6>(), mix_entry<7>(),
+                                             mix_entry<8>()};
+  return reg;
+}
+
+int grid_for(int64_t n, int threads, int num_sms) {
+  int64_t b = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms * 8));
+}
+
+// E-restriction of the H1 pressure space (mesh.py:157-164), rows padded to gs
+__global__ void mix_restriction_kernel(int* __restrict__ gids, int nx, int ny, int nz, int p,
+                                       int64_t npx, int64_t npy, int64_t gs) {
+  const int d = p + 1, d3 = d * d * d;
+  const int64_t total = (int64_t)nx * ny * nz * gs;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / gs;
+    const int l = (int)(t - e * gs);
+    if (l >= d3) {
+      gids[t] = 0;
+      continue;
+    }
+    const int i = l % d, j = (l / d) % d, k = l / (d * d);
+    const int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / ((int64_t)nx * ny);
+    gids[t] = (int)((ex * p + i) + npx * ((ey * p + j) + npy * (ez * p + k)));
+  }
+}
+
+// dmat (operator.py:137-144, 171-175): dm[e][s*3+r][qp] = wdet(qp) * Jinv[s][r]
+// with wdet = kron(w, kron(w, w)) * detJ and Jinv = diag(1/jac_diag).
+__global__ void mix_pa_kernel(double* __restrict__ pa, int64_t nel, int q, int64_t ps, double w0,
+                              double w1, double w2, double w3, double w4, double w5, double w6,
+                              double w7, double w8, double detj, double j0, double j1, double j2) {
+  const double w[9] = {w0, w1, w2, w3, w4, w5, w6, w7, w8};
+  const double jinv[3] = {j0, j1, j2};
+  const int q3 = q * q * q;
+  const int64_t total = nel * ps;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / ps;
+    const int k = (int)(t - e * ps);
+    double v = 0.0;
+    if (k < 9 * q3) {
+      const int comp = k / q3, qp = k - comp * q3;
+      const int s = comp / 3, r = comp % 3;
+      const int a = qp % q, b = (qp / q) % q, c = qp / (q * q);
+      if (s == r) v = (w[c] * (w[b] * w[a])) * detj * jinv[s];
+    }
+    pa[t] = v;
+  }
+}
+
+// lump_p = scatter_add(kinv[e] * lump_ref_p) (operator.py:185-188)
+__global__ void mix_lump_p_kernel(double* __restrict__ lump_p, const int* __restrict__ gids,
+                                  const double* __restrict__ kinv, const double* __restrict__ ref,
+                                  int64_t nel, int d3, int64_t gs) {
+  const int64_t total = nel * d3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / d3;
+    const int l = (int)(t - e * d3);
+    atomicAdd(lump_p + gids[e * gs + l], kinv[e] * ref[l]);
+  }
+}
+
+// lump_u[e][l] = rho[e] * lump_ref_u[l] (operator.py:184)
+__global__ void mix_lump_u_kernel(double* __restrict__ lump_u, const double* __restrict__ rho,
+                                  const double* __restrict__ ref, int64_t nel, int du3) {
+  const int64_t total = nel * du3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / du3;
+    lump_u[t] = rho[e] * ref[t - e * du3];
+  }
+}
+
+// k = -r / lump (rk4 rhs: negate, then apply_mass_inverse, operator.py:512-516)
+__global__ void mix_minv_kernel(double* __restrict__ ku, const double* __restrict__ ru,
+                                const double* __restrict__ lump_u, int64_t nu, int64_t nel_du3,
+                                double* __restrict__ kp, const double* __restrict__ rp,
+                                const double* __restrict__ lump_p, int64_t np, double sign) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nu + np;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < nu) ku[t] = (sign * ru[t]) / lump_u[t % nel_du3];
+    else kp[t - nu] = (sign * rp[t - nu]) / lump_p[t - nu];
+  }
+}
+
+// y = x + c k, two separately rounded operations like NumPy (state_lincomb)
+__global__ void mix_axpy_kernel(double* __restrict__ y, const double* __restrict__ x,
+                                const double* __restrict__ k, double c, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    y[t] = __dadd_rn(x[t], __dmul_rn(c, k[t]));
+}
+
+// y = (((y + c1 k1) + c2 k2) + c3 k3) + c4 k4 (the final lincomb, left to right)
+__global__ void mix_rk4_final_kernel(double* __restrict__ y, const double* __restrict__ k1,
+                                     const double* __restrict__ k2, const double* __restrict__ k3,
+                                     const double* __restrict__ k4, double c1, double c2, double c3,
+                                     double c4, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double v = __dadd_rn(y[t], __dmul_rn(c1, k1[t]));
+    v = __dadd_rn(v, __dmul_rn(c2, k2[t]));
+    v = __dadd_rn(v, __dmul_rn(c3, k3[t]));
+    y[t] = __dadd_rn(v, __dmul_rn(c4, k4[t]));
+  }
+}
+
+// sum_i x_i m[a][i], ascending i, separately rounded (contract_cyclic, tensor.py:177-210)
+void host_chain_t(const double* m /* q x d row-major: m[a*d+i] */, int q, int d, std::vector<double>& x,
+                  int n0, int n1, int n2) {
+  // one cyclic stage with M^T (d x q): out(j,k,i') = sum_a M[a][i'] x(a,j,k)
+  std::vector<double> out((size_t)n1 * n2 * d, 0.0);
+  for (int jk = 0; jk < n1 * n2; ++jk)
+    for (int ip = 0; ip < d; ++ip) {
+      double acc = 0.0;
+      for (int a = 0; a < n0; ++a) acc = acc + x[(size_t)jk * n0 + a] * m[a * d + ip];
+      out[(size_t)ip * n1 * n2 + jk] = acc;
+    }
+  x.swap(out);
+  (void)q;
+}
+
+}  // namespace
+
+struct fk_mix {
+  fk_mix_desc desc{};
+  int dp = 0, du = 0, q = 0;
+  int64_t nel = 0, ndof_p = 0, npx = 0, npy = 0;
+  std::vector<double> Bp, Gp, Bu, w, rho, kinv;
+  const MixKernel* kern = nullptr;
+  cudaStream_t stream = nullptr;
+  int device = 0, num_sms = 0, blocks = 0;
+  bool is_setup = false;
+  int* gids = nullptr;
+  double* pa = nullptr;
+  double* lump_u = nullptr;  // (nel, du^3)
+  double* lump_p = nullptr;  // ndof_p
+  double* zbuf = nullptr;    // fused-normal intermediate (ndof_p)
+  double* rk = nullptr;      // rk4 work: 4 stage vectors, stage state, residual, state
+  cudaEvent_t ev[4] = {};
+};
+
+namespace {
+
+int64_t nu_of(const fk_mix* m) { return 3 * m->nel * m->du * m->du * m->du; }
+
+int mix_launch_mode(fk_mix* m, const double* u, const double* p, double* out_u, double* out_p,
+                    int mode, double su, double sp, cudaStream_t s) {
+  MixArgs a;
+  a.p = p;
+  a.u = u;
+  a.out_u = out_u;
+  a.out_p = out_p;
+  a.gids = m->gids;
+  a.pa = m->pa;
+  a.su = su;
+  a.sp = sp;
+  a.nel = (int)m->nel;
+  m->kern->launch(*m->kern, m->Bp.data(), m->Gp.data(), m->Bu.data(), a, mode, m->blocks, s);
+  FK_CUDA(cudaGetLastError());
+  return FK_OK;
+}
+
+// out = A [u; p] (BlockOperator.apply): out_p zeroed, then one fused launch
+int mix_apply_dev(fk_mix* m, const double* u, const double* p, double* out_u, double* out_p,
+                  cudaStream_t s) {
+  FK_CUDA(cudaMemsetAsync(out_p, 0, sizeof(double) * m->ndof_p, s));
+  const double cs = m->desc.coupling_scale;
+  return mix_launch_mode(m, u, p, out_u, out_p, MIX_BOTH, cs, -cs, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int fk_mix_create(fk_mix** out, const fk_mix_desc* d) {
+  if (out == nullptr || d == nullptr) return fk_fail(FK_EINVAL, "null argument");
+  *out = nullptr;
+  // order_u >= 1: a GLL rule needs two points (tensor.py:29-41)
+  if (d->order_p < 2 || d->order_p > kMixMaxP)
+    return fk_fail(FK_EUNSUPPORTED, "order_p=%d outside 2..%d", d->order_p, kMixMaxP);
+  if (d->order_u != d->order_p - 1 || d->num_quad_1d != d->order_p + 1)
+    return fk_fail(FK_EUNSUPPORTED,
+                   "compiled spaces are H1(p) x L2(p-1) with q = p+1; got order_p=%d order_u=%d q=%d",
+                   d->order_p, d->order_u, d->num_quad_1d);
+  if (d->nx < 1 || d->ny < 1 || d->nz < 1)
+    return fk_fail(FK_EINVAL, "mesh dimensions %d x %d x %d do not match a box", d->nx, d->ny, d->nz);
+  if (!(d->jac_det > 0.0) || !(d->jac_diag[0] > 0.0) || !(d->jac_diag[1] > 0.0) ||
+      !(d->jac_diag[2] > 0.0))
+    return fk_fail(FK_EINVAL, "non-positive Jacobian determinant in element 0");
+  if (d->Bp == nullptr || d->Gp == nullptr || d->Bu == nullptr || d->w == nullptr)
+    return fk_fail(FK_EINVAL, "basis tables Bp, Gp, Bu, w are required");
+  fk_mix* m = new fk_mix();
+  m->desc = *d;
+  m->dp = d->order_p + 1;
+  m->du = d->order_u + 1;
+  m->q = d->num_quad_1d;
+  m->nel = (int64_t)d->nx * d->ny * d->nz;
+  m->npx = (int64_t)d->nx * d->order_p + 1;
+  m->npy = (int64_t)d->ny * d->order_p + 1;
+  m->ndof_p = m->npx * m->npy * ((int64_t)d->nz * d->order_p + 1);
+  if (m->ndof_p >= ((int64_t)1 << 31) || m->nel >= ((int64_t)1 << 31) - 64) {
+    delete m;
+    return fk_fail(FK_EINVAL, "problem too large for int32 dof ids");
+  }
+  m->Bp.assign(d->Bp, d->Bp + m->q * m->dp);
+  m->Gp.assign(d->Gp, d->Gp + m->q * m->dp);
+  m->Bu.assign(d->Bu, d->Bu + m->q * m->du);
+  m->w.assign(d->w, d->w + m->q);
+  m->rho.resize(m->nel);
+  m->kinv.resize(m->nel);
+  for (int64_t e = 0; e < m->nel; ++e) {
+    const double r = d->rho ? d->rho[e] : d->rho_scalar;
+    const double k = d->bulk ? d->bulk[e] : d->bulk_scalar;
+    if (!(r > 0.0) || !(k > 0.0)) {
+      delete m;
+      return fk_fail(FK_EINVAL, "density and bulk modulus must be positive");
+    }
+    m->rho[e] = r;
+    m->kinv[e] = 1.0 / k;
+  }
+  for (const auto& k : mix_registry())
+    if (k.dp == m->dp && k.du == m->du && k.q == m->q) m->kern = &k;
+  if (m->kern == nullptr) {
+    delete m;
+    return fk_fail(FK_EUNSUPPORTED, "no kernel for order_p=%d", d->order_p);
+  }
+  m->device = d->device;
+  m->stream = static_cast<cudaStream_t>(d->stream);
+  *out = m;
+  return FK_OK;
+}
+
+int fk_mix_setup(fk_mix* m) {
+  if (m == nullptr) return fk_fail(FK_EINVAL, "null handle");
+  FkDeviceGuard g(m->device);
+  cudaStream_t s = m->stream;
+  FK_CUDA(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->device));
+  const MixKernel& k = *m->kern;
+  const int dp3 = m->dp * m->dp * m->dp, du3 = m->du * m->du * m->du, q = m->q;
+  if (m->gids == nullptr) FK_CUDA(cudaMalloc(&m->gids, sizeof(int) * (m->nel * k.gs + 16)));
+  mix_restriction_kernel<<<grid_for(m->nel * k.gs, 256, m->num_sms), 256, 0, s>>>(
+      m->gids, m->desc.nx, m->desc.ny, m->desc.nz, m->desc.order_p, m->npx, m->npy, k.gs);
+  FK_CUDA(cudaGetLastError());
+  if (m->pa == nullptr) FK_CUDA(cudaMalloc(&m->pa, sizeof(double) * (m->nel * k.ps + 16)));
+  double w9[9] = {0};
+  for (int i = 0; i < q; ++i) w9[i] = m->w[i];
+  mix_pa_kernel<<<grid_for(m->nel * k.ps, 256, m->num_sms), 256, 0, s>>>(
+      m->pa, m->nel, q, k.ps, w9[0], w9[1], w9[2], w9[3], w9[4], w9[5], w9[6], w9[7], w9[8],
+      m->desc.jac_det, 1.0 / m->desc.jac_diag[0], 1.0 / m->desc.jac_diag[1],
+      1.0 / m->desc.jac_diag[2]);
+  FK_CUDA(cudaGetLastError());
+  // lumped diagonals: lump_ref = apply_basis_transpose_3d(basis, wdet_ref) on the host
+  std::vector<double> wdet((size_t)q * q * q);
+  for (int c = 0; c < q; ++c)
+    for (int b = 0; b < q; ++b)
+      for (int a = 0; a < q; ++a) wdet[a + q * (b + q * c)] = (m->w[c] * (m->w[b] * m->w[a])) * m->desc.jac_det;
+  auto lump_ref = [&](const std::vector<double>& B, int d) {
+    std::vector<double> x = wdet;
+    host_chain_t(B.data(), q, d, x, q, q, q);
+    host_chain_t(B.data(), q, d, x, q, q, d);
+    host_chain_t(B.data(), q, d, x, q, d, d);
+    return x;  // (d, d, d) x fastest
+  };
+  std::vector<double> lu = lump_ref(m->Bu, m->du), lp = lump_ref(m->Bp, m->dp);
+  double *d_ref = nullptr, *d_rho = nullptr, *d_kinv = nullptr;
+  FK_CUDA(cudaMalloc(&d_ref, sizeof(double) * (du3 + dp3)));
+  FK_CUDA(cudaMalloc(&d_rho, sizeof(double) * m->nel));
+  FK_CUDA(cudaMalloc(&d_kinv, sizeof(double) * m->nel));
+  FK_CUDA(cudaMemcpyAsync(d_ref, lu.data(), sizeof(double) * du3, cudaMemcpyHostToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(d_ref + du3, lp.data(), sizeof(double) * dp3, cudaMemcpyHostToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(d_rho, m->rho.data(), sizeof(double) * m->nel, cudaMemcpyHostToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(d_kinv, m->kinv.data(), sizeof(double) * m->nel, cudaMemcpyHostToDevice, s));
+  if (m->lump_u == nullptr) FK_CUDA(cudaMalloc(&m->lump_u, sizeof(double) * m->nel * du3));
+  if (m->lump_p == nullptr) FK_CUDA(cudaMalloc(&m->lump_p, sizeof(double) * m->ndof_p));
+  mix_lump_u_kernel<<<grid_for(m->nel * du3, 256, m->num_sms), 256, 0, s>>>(m->lump_u, d_rho, d_ref,
+                                                                            m->nel, du3);
+  FK_CUDA(cudaMemsetAsync(m->lump_p, 0, sizeof(double) * m->ndof_p, s));
+  mix_lump_p_kernel<<<grid_for(m->nel * dp3, 256, m->num_sms), 256, 0, s>>>(
+      m->lump_p, m->gids, d_kinv, d_ref + du3, m->nel, dp3, k.gs);
+  FK_CUDA(cudaGetLastError());
+  FK_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d_ref);
+  cudaFree(d_rho);
+  cudaFree(d_kinv);
+  for (const void* f : {k.f_both, k.f_tau, k.f_vb})
+    FK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
+  int occ = 0;
+  FK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.f_both, k.T, k.smem));
+  if (occ < 1) return fk_fail(FK_EUNSUPPORTED, "mixed kernel does not fit on an SM (smem %zu)", k.smem);
+  const int64_t nbatch = (m->nel + k.E - 1) / k.E;
+  m->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ * m->num_sms));
+  for (auto& e : m->ev) FK_CUDA(cudaEventCreate(&e));
+  m->is_setup = true;
+  return FK_OK;
+}
+
+int fk_mix_get_info(const fk_mix* m, fk_mix_info* info) {
+  if (m == nullptr || info == nullptr) return fk_fail(FK_EINVAL, "null argument");
+  info->nel = m->nel;
+  info->ndof_p = m->ndof_p;
+  info->ndof_u = nu_of(m);
+  info->pa_bytes = (int64_t)sizeof(double) * m->nel * m->kern->ps;
+  info->elems_per_block = m->kern->E;
+  info->threads_per_block = m->kern->T;
+  info->blocks = m->blocks;
+  info->smem_bytes = (int64_t)m->kern->smem;
+  return FK_OK;
+}
+
+int fk_mix_apply(fk_mix* m, const double* u, const double* p, double* out_u, double* out_p) {
+  if (m == nullptr || u == nullptr || p == nullptr || out_u == nullptr || out_p == nullptr)
+    return fk_fail(FK_EINVAL, "null argument");
+  if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
+  FkDeviceGuard g(m->device);
+  return mix_apply_dev(m, u, p, out_u, out_p, m->stream);
+}
+
+int fk_mix_fused_normal(fk_mix* m, const double* u, double* out_u) {
+  if (m == nullptr || u == nullptr || out_u == nullptr) return fk_fail(FK_EINVAL, "null argument");
+  if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
+  FkDeviceGuard g(m->device);
+  if (m->zbuf == nullptr) FK_CUDA(cudaMalloc(&m->zbuf, sizeof(double) * m->ndof_p));
+  FK_CUDA(cudaMemsetAsync(m->zbuf, 0, sizeof(double) * m->ndof_p, m->stream));
+  // z = sum_e G^T v_e(u) (operator.py:375-380), then out = tau(G z) (:381-386)
+  FK_TRY(mix_launch_mode(m, u, nullptr, nullptr, m->zbuf, MIX_VB, 1.0, 1.0, m->stream));
+  return mix_launch_mode(m, nullptr, m->zbuf, out_u, nullptr, MIX_TAU, 1.0, 1.0, m->stream);
+}
+
+int fk_mix_mass_inverse(fk_mix* m, const double* ru, const double* rp, double* u, double* p) {
+  if (m == nullptr || ru == nullptr || rp == nullptr || u == nullptr || p == nullptr)
+    return fk_fail(FK_EINVAL, "null argument");
+  if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
+  FkDeviceGuard g(m->device);
+  const int64_t nu = nu_of(m), du3 = m->du * m->du * m->du;
+  mix_minv_kernel<<<grid_for(nu + m->ndof_p, 256, m->num_sms), 256, 0, m->stream>>>(
+      u, ru, m->lump_u, nu, m->nel * du3, p, rp, m->lump_p, m->ndof_p, 1.0);
+  FK_CUDA(cudaGetLastError());
+  return FK_OK;
+}
+
+int fk_mix_rk4(fk_mix* m, double* u, double* p, double dt, int steps) {
+  if (m == nullptr || u == nullptr || p == nullptr) return fk_fail(FK_EINVAL, "null argument");
+  if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
+  if (!(dt > 0.0)) return fk_fail(FK_EINVAL, "dt must be positive, got %g", dt);
+  if (steps < 0) return fk_fail(FK_EINVAL, "steps must be >= 0");
+  FkDeviceGuard g(m->device);
+  const int64_t nu = nu_of(m), n = nu + m->ndof_p, du3 = m->du * m->du * m->du;
+  // state layout [u | p] in one buffer per stage vector
+  if (m->rk == nullptr) FK_CUDA(cudaMalloc(&m->rk, sizeof(double) * 7 * n));
+  double* k[4] = {m->rk, m->rk + n, m->rk + 2 * n, m->rk + 3 * n};
+  double* tmp = m->rk + 4 * n;
+  double* res = m->rk + 5 * n;
+  cudaStream_t s = m->stream;
+  const int gb = grid_for(n, 256, m->num_sms);
+  auto rhs = [&](const double* yu, const double* yp, double* kk) -> int {
+    FK_TRY(mix_apply_dev(m, yu, yp, res, res + nu, s));
+    mix_minv_kernel<<<gb, 256, 0, s>>>(kk, res, m->lump_u, nu, m->nel * du3, kk + nu, res + nu,
+                                        m->lump_p, m->ndof_p, -1.0);
+    FK_CUDA(cudaGetLastError());
+    return FK_OK;
+  };
+  // the state [u | p] lives in one work vector (u and p are separate user buffers)
+  double* y = tmp;
+  double* ybuf = m->rk + 6 * n;
+  FK_CUDA(cudaMemcpyAsync(ybuf, u, sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(ybuf + nu, p, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice, s));
+  for (int st = 0; st < steps; ++st) {
+    FK_TRY(rhs(ybuf, ybuf + nu, k[0]));
+    mix_axpy_kernel<<<gb, 256, 0, s>>>(y, ybuf, k[0], dt / 2, n);
+    FK_TRY(rhs(y, y + nu, k[1]));
+    mix_axpy_kernel<<<gb, 256, 0, s>>>(y, ybuf, k[1], dt / 2, n);
+    FK_TRY(rhs(y, y + nu, k[2]));
+    mix_axpy_kernel<<<gb, 256, 0, s>>>(y, ybuf, k[2], dt, n);
+    FK_TRY(rhs(y, y + nu, k[3]));
+    mix_rk4_final_kernel<<<gb, 256, 0, s>>>(ybuf, k[0], k[1], k[2], k[3], dt / 6, dt / 3, dt / 3,
+                                             dt / 6, n);
+    FK_CUDA(cudaGetLastError());
+  }
+  FK_CUDA(cudaMemcpyAsync(u, ybuf, sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(p, ybuf + nu, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice, s));
+  return FK_OK;
+}
+
+int fk_mix_lumped(fk_mix* m, double* lump_u, double* lump_p) {
+  if (m == nullptr || lump_u == nullptr || lump_p == nullptr) return fk_fail(FK_EINVAL, "null argument");
+  if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
+  FkDeviceGuard g(m->device);
+  const int64_t du3 = m->du * m->du * m->du;
+  FK_CUDA(cudaMemcpyAsync(lump_u, m->lump_u, sizeof(double) * m->nel * du3, cudaMemcpyDeviceToDevice,
+                          m->stream));
+  FK_CUDA(cudaMemcpyAsync(lump_p, m->lump_p, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice,
+                          m->stream));
+  return FK_OK;
+}
+
+int fk_mix_restriction(fk_mix* m, int64_t* host_out) {
+  if (m == nullptr || host_out == nullptr) return fk_fail(FK_EINVAL, "null argument");
+  if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
+  FkDeviceGuard g(m->device);
+  const int dp3 = m->dp * m->dp * m->dp, gs = m->kern->gs;
+  std::vector<int> buf((size_t)m->nel * gs);
+  FK_CUDA(cudaMemcpyAsync(buf.data(), m->gids, sizeof(int) * buf.size(), cudaMemcpyDeviceToHost, m->stream));
+  FK_CUDA(cudaStreamSynchronize(m->stream));
+  for (int64_t e = 0; e < m->nel; ++e)
+    for (int l = 0; l < dp3; ++l) host_out[e * dp3 + l] = buf[(size_t)e * gs + l];
+  return FK_OK;
+}
+
+int fk_mix_time_apply(fk_mix* m, const double* u, const double* p, double* out_u, double* out_p,
+                      int reps, double* ms_apply, double* ms_kernel) {
+  if (m == nullptr || reps < 1) return fk_fail(FK_EINVAL, "bad argument");
+  if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
+  FkDeviceGuard g(m->device);
+  std::vector<cudaEvent_t> ev(3 * (size_t)reps);
+  for (auto& e : ev) FK_CUDA(cudaEventCreate(&e));
+  const double cs = m->desc.coupling_scale;
+  for (int r = 0; r < reps; ++r) {
+    FK_CUDA(cudaEventRecord(ev[3 * r], m->stream));
+    FK_CUDA(cudaMemsetAsync(out_p, 0, sizeof(double) * m->ndof_p, m->stream));
+    FK_CUDA(cudaEventRecord(ev[3 * r + 1], m->stream));
+    FK_TRY(mix_launch_mode(m, u, p, out_u, out_p, MIX_BOTH, cs, -cs, m->stream));
+    FK_CUDA(cudaEventRecord(ev[3 * r + 2], m->stream));
+  }
+  FK_CUDA(cudaEventSynchronize(ev.back()));
+  double ta = 0.0, tk = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    float a = 0.f, k = 0.f;
+    FK_CUDA(cudaEventElapsedTime(&a, ev[3 * r], ev[3 * r + 2]));
+    FK_CUDA(cudaEventElapsedTime(&k, ev[3 * r + 1], ev[3 * r + 2]));
+    ta += a;
+    tk += k;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (ms_apply) *ms_apply = ta / reps;
+  if (ms_kernel) *ms_kernel = tk / reps;
+  return FK_OK;
+}
+
+int fk_mix_destroy(fk_mix* m) {
+  if (m == nullptr) return FK_OK;
+  FkDeviceGuard g(m->device);
+  cudaFree(m->gids);
+  cudaFree(m->pa);
+  cudaFree(m->lump_u);
+  cudaFree(m->lump_p);
+  cudaFree(m->zbuf);
+  cudaFree(m->rk);
+  for (auto& e : m->ev)
+    if (e) cudaEventDestroy(e);
+  delete m;
+  return FK_OK;
+}
+
+}  // extern "C"

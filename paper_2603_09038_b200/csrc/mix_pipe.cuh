@@ -1,0 +1,432 @@
+// mix_pipe.cuh — fused partial-assembly apply of the acoustic-gravity block
+// operator (feklab/operator.py BlockOperator, strategy FusedPA):
+//
+//   out_u[r, e] = su * B_u^T (sum_s D[s][r] (grad_ref p)_s)     tau block, :288-301
+//   out_p     += sp * G^T (grad_ref^T (sum_r D[s][r] B_u u_r))  v block,   :303-319
+//
+// p: continuous H1 space of order DP-1 (global dofs, gathered/scattered
+// through the E-restriction, mesh.py:130-137); u: 3 discontinuous L2
+// components of order DU-1 (element blocks (3, nel, DU^3)); D = dmat
+// (operator.py:105-123, 137-144) stored as 9 components [s*3+r][qp].  Both
+// blocks contract the same quadrature data, so one pass reads D once (the
+// paper's "Fused PA").  TAU / VB select the blocks (the composed normal
+// operator apply_fused_normal, :364-387, runs VB then TAU).
+//
+// Dataflow per element (thread per line, even-odd folded FP64 FMA as in
+// pa_dfma_eo.cuh; x, y, z = the reference's cyclic stage order):
+//   A  x:  p lines (j,k) -> B_p x, G_p x          u lines (r,j,k) -> B_u x
+//   B  y:  p lines (a,k) -> 3 gradient chains      u lines (r,a,k) -> B_u y
+//   C  z + D + z^T, lines (a,b):
+//        P phase: grad p at the points, t_r = sum_s D_sr g_s, B_u^T z -> W_u
+//        U phase: u at the points,  t_s = sum_r D_sr u_r, (B_p^T,B_p^T,G_p^T) z -> W_p
+//   D  y^T: u lines (r,a,k) B_u^T                   p lines (a,k): rG = B^T W0, rB = G^T W1 + B^T W2
+//   E  x^T: u lines (r,j,k) B_u^T -> out_u (stores) p lines (j,k): G^T rG + B^T rB -> atomics
+// Persistent CTAs with the pa_pipe.cuh prefetch pattern: the next batch's p
+// gather and u block (cp.async) and gids (bulk copy, three slots) are in
+// flight during the current batch, D(b+1) is bulk-copied after stage C(b).
+#pragma once
+
+#include "pa_async.cuh"
+#include "pa_common.cuh"
+#include "pa_dfma_eo.cuh"
+
+namespace fk {
+
+template <int DP, int DU, int Q>
+struct __align__(16) MixTables {
+  using FBp = Fold<Q, DP>;
+  using FBpT = Fold<DP, Q>;
+  using FBu = Fold<Q, DU>;
+  using FBuT = Fold<DU, Q>;
+  static constexpr int TBP = 0, TGP = FBp::SIZE, TBPT = 2 * FBp::SIZE, TGPT = TBPT + FBpT::SIZE;
+  static constexpr int TBU = TGPT + FBpT::SIZE, TBUT = TBU + FBu::SIZE, SZ = TBUT + FBuT::SIZE;
+  double t[SZ];
+
+  // host: fold the reference tables (row-major q x d)
+  void fill(const double* Bp, const double* Gp, const double* Bu) {
+    double BpT[Q * DP], GpT[Q * DP], BuT[Q * DU];
+    for (int a = 0; a < Q; ++a) {
+      for (int i = 0; i < DP; ++i) {
+        BpT[i * Q + a] = Bp[a * DP + i];
+        GpT[i * Q + a] = Gp[a * DP + i];
+      }
+      for (int i = 0; i < DU; ++i) BuT[i * Q + a] = Bu[a * DU + i];
+    }
+    fold_table<Q, DP>(t + TBP, Bp, +1);
+    fold_table<Q, DP>(t + TGP, Gp, -1);
+    fold_table<DP, Q>(t + TBPT, BpT, +1);
+    fold_table<DP, Q>(t + TGPT, GpT, -1);
+    fold_table<Q, DU>(t + TBU, Bu, +1);
+    fold_table<DU, Q>(t + TBUT, BuT, +1);
+  }
+};
+
+// Shared-memory and global layouts of one (DP, DU, Q) instance.
+template <int DP, int DU, int Q>
+struct MixLayout {
+  static constexpr int LSP = DP | 1, LSU = DU | 1, LQ = Q | 1;
+  static constexpr int DP3 = DP * DP * DP, DU3 = DU * DU * DU, Q3 = Q * Q * Q;
+  // X buffers
+  static constexpr int XPS = odd_up(DP * DP * LSP);
+  static constexpr int XUC = DU * DU * LSU, XUS = odd_up(3 * XUC);
+  __device__ __forceinline__ static int xp(int e, int i, int j, int k) { return e * XPS + i + LSP * (j + DP * k); }
+  __device__ __forceinline__ static int xu(int e, int r, int i, int j, int k) {
+    return e * XUS + r * XUC + i + LSU * (j + DU * k);
+  }
+  // region 1: T1p (2), T1u (3), later Wp (3), Wu (3)
+  static constexpr int T1PC = Q * DP * LSP, T1UC = Q * DU * LSU, OFF_T1U = 2 * T1PC;
+  static constexpr int WPC = DP * Q * LQ, WUC = DU * Q * LQ, OFF_WU = 3 * WPC;
+  static constexpr int R1S = odd_up(cmax(2 * T1PC + 3 * T1UC, 3 * WPC + 3 * WUC));
+  __device__ __forceinline__ static int t1p(int e, int s, int a, int j, int k) {
+    return e * R1S + s * T1PC + a * DP * LSP + j + LSP * k;
+  }
+  __device__ __forceinline__ static int t1u(int e, int r, int a, int j, int k) {
+    return e * R1S + OFF_T1U + r * T1UC + a * DU * LSU + j + LSU * k;
+  }
+  __device__ __forceinline__ static int wp(int e, int s, int a, int b, int k) {
+    return e * R1S + s * WPC + a * LQ + b + Q * LQ * k;
+  }
+  __device__ __forceinline__ static int wu(int e, int r, int a, int b, int k) {
+    return e * R1S + OFF_WU + r * WUC + a * LQ + b + Q * LQ * k;
+  }
+  // region 0: T2p (3), T2u (3), later Rp (2), Ru (3)
+  static constexpr int T2PC = Q * Q * LSP, T2UC = Q * Q * LSU, OFF_T2U = 3 * T2PC;
+  static constexpr int RPC = DP * DP * LQ, RUC = DU * DU * LQ, OFF_RU = 2 * RPC;
+  static constexpr int R0S = odd_up(cmax(3 * T2PC + 3 * T2UC, 2 * RPC + 3 * RUC));
+  __device__ __forceinline__ static int t2p(int e, int s, int a, int b, int k) {
+    return e * R0S + s * T2PC + a * LSP + Q * LSP * b + k;
+  }
+  __device__ __forceinline__ static int t2u(int e, int r, int a, int b, int k) {
+    return e * R0S + OFF_T2U + r * T2UC + a * LSU + Q * LSU * b + k;
+  }
+  __device__ __forceinline__ static int rp(int e, int s, int a, int j, int k) {
+    return e * R0S + s * RPC + a + LQ * j + DP * LQ * k;
+  }
+  __device__ __forceinline__ static int ru(int e, int r, int a, int j, int k) {
+    return e * R0S + OFF_RU + r * RUC + a + LQ * j + DU * LQ * k;
+  }
+  // global: PA data 9 components per point, int32 gather ids
+  static constexpr int PS = pa_pad(((9 * Q3 + 1) / 2) * 2, Q);
+  static constexpr int GS = ((DP3 + 3) / 4) * 4;
+};
+
+template <int DP, int DU, int Q, int E>
+struct MixSmem {
+  using L = MixLayout<DP, DU, Q>;
+  static constexpr size_t OFF_BAR = 0;  // 1 D barrier + 3 gid barriers
+  static constexpr size_t OFF_DB = 32;
+  static constexpr size_t OFF_GS = OFF_DB + 8ull * E * L::PS;
+  static constexpr size_t OFF_R0 = OFF_GS + 4ull * 3 * E * L::GS;
+  static constexpr size_t OFF_R1 = OFF_R0 + 8ull * E * L::R0S;
+  static constexpr size_t OFF_XP = OFF_R1 + 8ull * E * L::R1S;
+  static constexpr size_t OFF_XU = OFF_XP + 8ull * 2 * E * L::XPS;
+  static constexpr size_t BYTES = OFF_XU + 8ull * 2 * E * L::XUS;
+};
+
+struct MixArgs {
+  const double* p;  // H1 pressure dofs (TAU input)
+  const double* u;  // (3, nel, DU^3) velocity blocks (VB input)
+  double* out_u;    // (3, nel, DU^3), overwritten (TAU)
+  double* out_p;    // accumulated with atomics (VB)
+  const int* gids;
+  const double* pa;
+  double su, sp;  // output scales (coupling_scale, -coupling_scale for apply)
+  int nel;
+};
+
+template <int DP, int DU, int Q, int E, int T, bool TAU, bool VB>
+__global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ MixTables<DP, DU, Q> tb,
+                                                     const MixArgs arg) {
+  using L = MixLayout<DP, DU, Q>;
+  using S = MixSmem<DP, DU, Q, E>;
+  using Tb = MixTables<DP, DU, Q>;
+  constexpr int DP3 = L::DP3, DU3 = L::DU3, Q3 = L::Q3, GS = L::GS, PS = L::PS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar_d = reinterpret_cast<uint64_t*>(smem_raw + S::OFF_BAR);
+  uint64_t* bar_g = bar_d + 1;
+  double* db = reinterpret_cast<double*>(smem_raw + S::OFF_DB);
+  int* gs = reinterpret_cast<int*>(smem_raw + S::OFF_GS);
+  double* s0 = reinterpret_cast<double*>(smem_raw + S::OFF_R0);
+  double* s1 = reinterpret_cast<double*>(smem_raw + S::OFF_R1);
+  double* xpb = reinterpret_cast<double*>(smem_raw + S::OFF_XP);
+  double* xub = reinterpret_cast<double*>(smem_raw + S::OFF_XU);
+  const double* tab = tb.t;
+  const int nel = arg.nel;
+  const int nbatch = (nel + E - 1) / E;
+  if ((int)blockIdx.x >= nbatch) return;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_d, 1);
+    for (int s = 0; s < 3; ++s) mbar_init(bar_g + s, 1);
+    fence_mbar_init();
+  }
+  for (size_t i = threadIdx.x; i < (S::BYTES - S::OFF_R0) / 8; i += T)
+    reinterpret_cast<double*>(smem_raw + S::OFF_R0)[i] = 0.0;
+  __syncthreads();
+
+  auto issue_g = [&](int b, int slot) {
+    const int e0 = b * E, ne = min(E, nel - e0);
+    const uint32_t bytes = 4u * ne * GS;
+    mbar_expect_tx(bar_g + slot, bytes);
+    bulk_g2s(gs + slot * E * GS, arg.gids + (size_t)e0 * GS, bytes, bar_g + slot);
+  };
+  auto issue_d = [&](int b) {
+    const int e0 = b * E, ne = min(E, nel - e0);
+    const uint32_t bytes = 8u * ne * PS;
+    mbar_expect_tx(bar_d, bytes);
+    bulk_g2s(db, arg.pa + (size_t)e0 * PS, bytes, bar_d);
+  };
+  // p gather (TAU) and u block (VB) of batch b into X buffer half `h`
+  auto issue_x = [&](int b, int gslot, int h) {
+    const int e0 = b * E, ne = min(E, nel - e0);
+    if constexpr (TAU) {
+      const int* g = gs + gslot * E * GS;
+      double* xp = xpb + h * E * L::XPS;
+      for (int t = threadIdx.x; t < E * DP3; t += T) {
+        const int e = t / DP3, l = t - e * DP3;
+        double* dst = xp + L::xp(e, l % DP, (l / DP) % DP, l / (DP * DP));
+        if (e < ne) cp_async8(dst, arg.p + g[e * GS + l]);
+        else *dst = 0.0;
+      }
+    }
+    if constexpr (VB) {
+      double* xu = xub + h * E * L::XUS;
+      for (int t = threadIdx.x; t < 3 * E * DU3; t += T) {
+        const int r = t / (E * DU3), m = t - r * (E * DU3), e = m / DU3, l = m - e * DU3;
+        double* dst = xu + L::xu(e, r, l % DU, (l / DU) % DU, l / (DU * DU));
+        if (e < ne) cp_async8(dst, arg.u + ((size_t)r * nel + e0 + e) * DU3 + l);
+        else *dst = 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+  uint32_t ph_g = 0u, ph_d = 0u;
+  auto wait_g = [&](int slot) {
+    mbar_wait(bar_g + slot, (ph_g >> slot) & 1u);
+    ph_g ^= 1u << slot;
+  };
+  // element-major thread -> (e, line) loop over a stage's lines
+  auto lines = [&](int ne, int nl, auto f) {
+    for (int t = threadIdx.x; t < E * nl; t += T) {
+      const int e = t / nl, l = t - e * nl;
+      if (e < ne) f(e, l);
+    }
+  };
+  constexpr int NAP = TAU ? DP * DP : 0, NAU = VB ? 3 * DU * DU : 0;
+  constexpr int NBP = TAU ? Q * DP : 0, NBU = VB ? 3 * Q * DU : 0;
+  constexpr int NCP = TAU ? Q * Q : 0, NCU = VB ? Q * Q : 0;
+  constexpr int NDU = TAU ? 3 * Q * DU : 0, NDP = VB ? Q * DP : 0;
+
+  const int stride = (int)gridDim.x;
+  if (threadIdx.x == 0) {
+    issue_g(blockIdx.x, 0);
+    if ((int)blockIdx.x + stride < nbatch) issue_g(blockIdx.x + stride, 1);
+    issue_d(blockIdx.x);
+  }
+  wait_g(0);
+  issue_x(blockIdx.x, 0, 0);
+
+  int it = 0;
+  for (int b = blockIdx.x; b < nbatch; b += stride, ++it) {
+    const int gslot = it % 3, h = it & 1;
+    const int e0 = b * E, ne = min(E, nel - e0);
+    const int nb = b + stride, nb2 = nb + stride;
+    const double* xp = xpb + h * E * L::XPS;
+    const double* xu = xub + h * E * L::XUS;
+    cp_async_wait_all();
+    __syncthreads();
+    if (nb < nbatch) {
+      wait_g((it + 1) % 3);
+      issue_x(nb, (it + 1) % 3, h ^ 1);
+      if (nb2 < nbatch && threadIdx.x == 0) {
+        fence_proxy_async();
+        issue_g(nb2, (it + 2) % 3);
+      }
+    }
+    // ---- stage A: x contraction
+    lines(ne, NAP + NAU, [&](int e, int l) {
+      if (TAU && l < NAP) {
+        const int j = l % DP, k = l / DP;
+        double xr[DP], o[Q];
+#pragma unroll
+        for (int i = 0; i < DP; ++i) xr[i] = xp[L::xp(e, i, j, k)];
+        contract_eo<DP, Q, +1>(tab + Tb::TBP, xr, o);
+#pragma unroll
+        for (int a = 0; a < Q; ++a) s1[L::t1p(e, 0, a, j, k)] = o[a];
+        contract_eo<DP, Q, -1>(tab + Tb::TGP, xr, o);
+#pragma unroll
+        for (int a = 0; a < Q; ++a) s1[L::t1p(e, 1, a, j, k)] = o[a];
+      } else if (VB) {
+        const int m = l - NAP, r = m / (DU * DU), jk = m - r * (DU * DU), j = jk % DU, k = jk / DU;
+        double xr[DU], o[Q];
+#pragma unroll
+        for (int i = 0; i < DU; ++i) xr[i] = xu[L::xu(e, r, i, j, k)];
+        contract_eo<DU, Q, +1>(tab + Tb::TBU, xr, o);
+#pragma unroll
+        for (int a = 0; a < Q; ++a) s1[L::t1u(e, r, a, j, k)] = o[a];
+      }
+    });
+    __syncthreads();
+    // ---- stage B: y contraction
+    lines(ne, NBP + NBU, [&](int e, int l) {
+      if (TAU && l < NBP) {
+        const int a = l / DP, k = l % DP;
+        double bx[DP], gx[DP], c[Q];
+#pragma unroll
+        for (int j = 0; j < DP; ++j) {
+          bx[j] = s1[L::t1p(e, 0, a, j, k)];
+          gx[j] = s1[L::t1p(e, 1, a, j, k)];
+        }
+        contract_eo<DP, Q, +1>(tab + Tb::TBP, gx, c);  // B_y G_x
+#pragma unroll
+        for (int b2 = 0; b2 < Q; ++b2) s0[L::t2p(e, 0, a, b2, k)] = c[b2];
+        contract_eo<DP, Q, -1>(tab + Tb::TGP, bx, c);  // G_y B_x
+#pragma unroll
+        for (int b2 = 0; b2 < Q; ++b2) s0[L::t2p(e, 1, a, b2, k)] = c[b2];
+        contract_eo<DP, Q, +1>(tab + Tb::TBP, bx, c);  // B_y B_x
+#pragma unroll
+        for (int b2 = 0; b2 < Q; ++b2) s0[L::t2p(e, 2, a, b2, k)] = c[b2];
+      } else if (VB) {
+        const int m = l - NBP, r = m / (Q * DU), ak = m - r * (Q * DU), a = ak / DU, k = ak % DU;
+        double v[DU], c[Q];
+#pragma unroll
+        for (int j = 0; j < DU; ++j) v[j] = s1[L::t1u(e, r, a, j, k)];
+        contract_eo<DU, Q, +1>(tab + Tb::TBU, v, c);
+#pragma unroll
+        for (int b2 = 0; b2 < Q; ++b2) s0[L::t2u(e, r, a, b2, k)] = c[b2];
+      }
+    });
+    __syncthreads();
+    // ---- stage C: z + D + z^T (D read once for both blocks)
+    mbar_wait(bar_d, ph_d);
+    ph_d ^= 1u;
+    lines(ne, NCP + NCU, [&](int e, int l) {
+      const bool pph = TAU && l < NCP;
+      const int m = pph ? l : l - NCP;
+      const int a = m % Q, b2 = m / Q;
+      const double* pe = db + e * PS + a + Q * b2;
+      if (TAU && pph) {
+        double tin[3][DP], g0[Q], g1[Q], g2[Q];
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+          for (int k = 0; k < DP; ++k) tin[s][k] = s0[L::t2p(e, s, a, b2, k)];
+        contract_eo<DP, Q, +1>(tab + Tb::TBP, tin[0], g0);
+        contract_eo<DP, Q, +1>(tab + Tb::TBP, tin[1], g1);
+        contract_eo<DP, Q, -1>(tab + Tb::TGP, tin[2], g2);
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+          const double* pc = pe + c * Q * Q;
+          const double x0 = g0[c], x1 = g1[c], x2 = g2[c];
+          // t_r = sum_s D[s][r] g_s  (einsum qsr,sq->rq, operator.py:294)
+          g0[c] = fma(pc[6 * Q3], x2, fma(pc[3 * Q3], x1, pc[0 * Q3] * x0));
+          g1[c] = fma(pc[7 * Q3], x2, fma(pc[4 * Q3], x1, pc[1 * Q3] * x0));
+          g2[c] = fma(pc[8 * Q3], x2, fma(pc[5 * Q3], x1, pc[2 * Q3] * x0));
+        }
+        double w[DU];
+        contract_eo<Q, DU, +1>(tab + Tb::TBUT, g0, w);
+#pragma unroll
+        for (int k = 0; k < DU; ++k) s1[L::wu(e, 0, a, b2, k)] = w[k];
+        contract_eo<Q, DU, +1>(tab + Tb::TBUT, g1, w);
+#pragma unroll
+        for (int k = 0; k < DU; ++k) s1[L::wu(e, 1, a, b2, k)] = w[k];
+        contract_eo<Q, DU, +1>(tab + Tb::TBUT, g2, w);
+#pragma unroll
+        for (int k = 0; k < DU; ++k) s1[L::wu(e, 2, a, b2, k)] = w[k];
+      } else if (VB) {
+        double tin[3][DU], u0[Q], u1[Q], u2[Q];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int k = 0; k < DU; ++k) tin[r][k] = s0[L::t2u(e, r, a, b2, k)];
+        contract_eo<DU, Q, +1>(tab + Tb::TBU, tin[0], u0);
+        contract_eo<DU, Q, +1>(tab + Tb::TBU, tin[1], u1);
+        contract_eo<DU, Q, +1>(tab + Tb::TBU, tin[2], u2);
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+          const double* pc = pe + c * Q * Q;
+          const double x0 = u0[c], x1 = u1[c], x2 = u2[c];
+          // t_s = sum_r D[s][r] u_r  (einsum qsr,rq->sq, operator.py:316)
+          u0[c] = fma(pc[2 * Q3], x2, fma(pc[1 * Q3], x1, pc[0 * Q3] * x0));
+          u1[c] = fma(pc[5 * Q3], x2, fma(pc[4 * Q3], x1, pc[3 * Q3] * x0));
+          u2[c] = fma(pc[8 * Q3], x2, fma(pc[7 * Q3], x1, pc[6 * Q3] * x0));
+        }
+        double w[DP];
+        contract_eo<Q, DP, +1>(tab + Tb::TBPT, u0, w);
+#pragma unroll
+        for (int k = 0; k < DP; ++k) s1[L::wp(e, 0, a, b2, k)] = w[k];
+        contract_eo<Q, DP, +1>(tab + Tb::TBPT, u1, w);
+#pragma unroll
+        for (int k = 0; k < DP; ++k) s1[L::wp(e, 1, a, b2, k)] = w[k];
+        contract_eo<Q, DP, -1>(tab + Tb::TGPT, u2, w);
+#pragma unroll
+        for (int k = 0; k < DP; ++k) s1[L::wp(e, 2, a, b2, k)] = w[k];
+      }
+    });
+    __syncthreads();
+    if (nb < nbatch && threadIdx.x == 0) {
+      fence_proxy_async();
+      issue_d(nb);
+    }
+    // ---- stage D: y^T
+    lines(ne, NDU + NDP, [&](int e, int l) {
+      if (TAU && l < NDU) {
+        const int r = l / (Q * DU), ak = l - r * (Q * DU), a = ak % Q, k = ak / Q;
+        double v[Q], o[DU];
+#pragma unroll
+        for (int b2 = 0; b2 < Q; ++b2) v[b2] = s1[L::wu(e, r, a, b2, k)];
+        contract_eo<Q, DU, +1>(tab + Tb::TBUT, v, o);
+#pragma unroll
+        for (int j = 0; j < DU; ++j) s0[L::ru(e, r, a, j, k)] = o[j];
+      } else if (VB) {
+        const int m = l - NDU, a = m % Q, k = m / Q;
+        double v[Q], r0[DP], r1[DP];
+#pragma unroll
+        for (int b2 = 0; b2 < Q; ++b2) v[b2] = s1[L::wp(e, 0, a, b2, k)];
+        contract_eo<Q, DP, +1>(tab + Tb::TBPT, v, r0);  // rG = B^T W0
+#pragma unroll
+        for (int j = 0; j < DP; ++j) s0[L::rp(e, 0, a, j, k)] = r0[j];
+#pragma unroll
+        for (int b2 = 0; b2 < Q; ++b2) v[b2] = s1[L::wp(e, 1, a, b2, k)];
+        contract_eo<Q, DP, -1>(tab + Tb::TGPT, v, r0);  // G^T W1
+#pragma unroll
+        for (int b2 = 0; b2 < Q; ++b2) v[b2] = s1[L::wp(e, 2, a, b2, k)];
+        contract_eo<Q, DP, +1>(tab + Tb::TBPT, v, r1);  // B^T W2
+#pragma unroll
+        for (int j = 0; j < DP; ++j) s0[L::rp(e, 1, a, j, k)] = r0[j] + r1[j];
+      }
+    });
+    __syncthreads();
+    // ---- stage E: x^T, outputs
+    const int* g = gs + gslot * E * GS;
+    constexpr int NEU = TAU ? 3 * DU * DU : 0, NEP = VB ? DP * DP : 0;
+    lines(ne, NEU + NEP, [&](int e, int l) {
+      if (TAU && l < NEU) {
+        const int r = l / (DU * DU), jk = l - r * (DU * DU), j = jk % DU, k = jk / DU;
+        double v[Q], o[DU];
+#pragma unroll
+        for (int a = 0; a < Q; ++a) v[a] = s0[L::ru(e, r, a, j, k)];
+        contract_eo<Q, DU, +1>(tab + Tb::TBUT, v, o);
+        double* dst = arg.out_u + ((size_t)r * nel + e0 + e) * DU3 + DU * (j + DU * k);
+#pragma unroll
+        for (int i = 0; i < DU; ++i) dst[i] = arg.su * o[i];
+      } else if (VB) {
+        const int m = l - NEU, j = m % DP, k = m / DP;
+        double v[Q], o[DP], o2[DP];
+#pragma unroll
+        for (int a = 0; a < Q; ++a) v[a] = s0[L::rp(e, 0, a, j, k)];
+        contract_eo<Q, DP, -1>(tab + Tb::TGPT, v, o);  // G^T rG
+#pragma unroll
+        for (int a = 0; a < Q; ++a) v[a] = s0[L::rp(e, 1, a, j, k)];
+        contract_eo<Q, DP, +1>(tab + Tb::TBPT, v, o2);  // B^T rB
+        const int* ge = g + e * GS + DP * (j + DP * k);
+#pragma unroll
+        for (int i = 0; i < DP; ++i) atomicAdd(arg.out_p + ge[i], arg.sp * (o[i] + o2[i]));
+      }
+    });
+    // the next iteration's barrier (after its cp.async wait) orders stage E
+    // reads of R and of this gid slot before anything overwrites them
+  }
+}
+
+}  // namespace fk

@@ -1,0 +1,272 @@
+"""Acoustic-gravity block operator on B200.
+
+Drop-in sibling of ``feklab.operator.BlockOperator`` (operator.py:221-397)
+for the FusedPA / PA strategies: the coupled first-order wave operator with a
+continuous H1 pressure (``order_p``) and discontinuous L2 velocity
+(``order_u``), evaluated by one fused sm_100a kernel per apply that reads the
+quadrature factors ``dmat`` once for both off-diagonal blocks
+(libfk_b200.so, ``fk_mix_*`` in include/fk.h).  ``rk4_step`` mirrors
+operator.py:506-531 and ``MixedOperator.rk4`` runs whole steps on the device.
+
+States are ``State(u, p)`` with ``u`` of shape (3, nel, (order_u+1)^3) and
+``p`` of length ``num_p`` — NumPy arrays (host; copied in and out) or CUDA
+float64 tensors (stay on the device); the reference's own ``State`` objects
+are accepted (duck-typed ``.u`` / ``.p``).  No CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .fem import Basis1D, Counters, h1_gather_ids
+
+STRATEGIES = ("PA", "FusedPA")
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class DivergenceError(FloatingPointError):
+    """Time stepping produced non-finite values (operator.py:52-53)."""
+
+
+@dataclass
+class State:
+    """Velocity blocks (3, elements, local dofs) plus pressure dofs (operator.py:63-90)."""
+
+    u: object
+    p: object
+
+    def copy(self) -> "State":
+        return State(self.u.copy() if isinstance(self.u, np.ndarray) else self.u.clone(),
+                     self.p.copy() if isinstance(self.p, np.ndarray) else self.p.clone())
+
+    @property
+    def num_dofs(self) -> int:
+        return int(np.prod(self.u.shape)) + int(self.p.shape[0])
+
+
+class MixedOperator:
+    """``BlockOperator(mesh, order_p, order_u, num_quad_1d, strategy, ...)`` on B200.
+
+    Supported: order_u = order_p - 1, num_quad_1d = order_p + 1, order_p = 2..8
+    (the reference default 4/3/5), scalar or per-element rho / bulk modulus,
+    coupling_scale.  Not supported (raise): absorbing faces, surface gravity,
+    the "MF"/"FusedMF" strategies (operator.py:400-440, :280-286).
+    """
+
+    def __init__(self, mesh, order_p: int = 4, order_u: int = 3, num_quad_1d: int = 5,
+                 strategy: str = "FusedPA", rho=1.0, bulk_modulus=1.0,
+                 coupling_scale: float = 1.0, absorbing: bool = False,
+                 surface_gravity=None, counters: Counters | None = None, device=None,
+                 stream=None):
+        if strategy not in STRATEGIES:
+            raise ValueError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
+        if absorbing or surface_gravity is not None:
+            raise NotImplementedError("absorbing faces / surface gravity are not on the B200 path")
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("MixedOperator needs a CUDA device (there is no CPU fallback)")
+        lib = _lib.load()
+        self._lib = lib
+        self.mesh = mesh
+        self.strategy = strategy
+        self.coupling_scale = float(coupling_scale)
+        self.counters = counters if counters is not None else Counters()
+        self.basis_p = Basis1D.nodal(order_p + 1, num_quad_1d)
+        self.basis_u = Basis1D.nodal(order_u + 1, num_quad_1d)
+        self.order_p, self.order_u, self.num_quad_1d = int(order_p), int(order_u), int(num_quad_1d)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        with torch.cuda.device(self.device):
+            self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        nel = mesh.nx * mesh.ny * mesh.nz
+        self._tabs = [np.ascontiguousarray(t, dtype=np.float64) for t in
+                      (self.basis_p.values, self.basis_p.gradients, self.basis_u.values,
+                       self.basis_p.quad_weights)]
+        rho_a = np.broadcast_to(np.asarray(rho, dtype=np.float64), (nel,)).copy()
+        bulk_a = np.broadcast_to(np.asarray(bulk_modulus, dtype=np.float64), (nel,)).copy()
+        if np.any(rho_a <= 0) or np.any(bulk_a <= 0):
+            raise ValueError("density and bulk modulus must be positive")
+        self._rho, self._bulk = rho_a, bulk_a
+        desc = _lib.FkMixDesc()
+        desc.order_p, desc.order_u, desc.num_quad_1d = self.order_p, self.order_u, self.num_quad_1d
+        desc.nx, desc.ny, desc.nz = mesh.nx, mesh.ny, mesh.nz
+        jd = np.asarray(mesh.jacobian_diag, dtype=np.float64)
+        for s in range(3):
+            desc.jac_diag[s] = float(jd[s])
+        desc.jac_det = float(mesh.jacobian_det)
+        pd = ctypes.POINTER(ctypes.c_double)
+        desc.Bp, desc.Gp, desc.Bu, desc.w = (t.ctypes.data_as(pd) for t in self._tabs)
+        desc.rho = rho_a.ctypes.data_as(pd)
+        desc.bulk = bulk_a.ctypes.data_as(pd)
+        desc.rho_scalar = desc.bulk_scalar = 1.0
+        desc.coupling_scale = self.coupling_scale
+        desc.device = self.device.index
+        desc.stream = ctypes.c_void_p(self._stream.cuda_stream)
+        h = ctypes.c_void_p()
+        _lib.check(lib.fk_mix_create(ctypes.byref(h), ctypes.byref(desc)))
+        self._h = h
+        _lib.check(lib.fk_mix_setup(self._h))
+        info = _lib.FkMixInfo()
+        _lib.check(lib.fk_mix_get_info(self._h, ctypes.byref(info)))
+        self.info = info
+        self.num_elements = int(info.nel)
+        self.num_p = int(info.ndof_p)
+        self.num_dofs_u_local = (self.order_u + 1) ** 3
+        self.num_dofs = int(info.ndof_u) + self.num_p
+        self._zero_u = None
+
+    # -- lifecycle ------------------------------------------------------------
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.fk_mix_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launch(self) -> tuple[int, int, int]:
+        return self.info.elems_per_block, self.info.threads_per_block, self.info.blocks
+
+    # -- states ---------------------------------------------------------------
+
+    @property
+    def u_shape(self) -> tuple[int, int, int]:
+        return (3, self.num_elements, self.num_dofs_u_local)
+
+    def zero_state(self, device: bool = False) -> State:
+        if device:
+            torch = _torch()
+            z = lambda *s: torch.zeros(*s, dtype=torch.float64, device=self.device)  # noqa: E731
+            return State(z(*self.u_shape), z(self.num_p))
+        return State(np.zeros(self.u_shape), np.zeros(self.num_p))
+
+    def _check(self, state) -> None:
+        u, p = state.u, state.p
+        if tuple(u.shape) != self.u_shape or tuple(p.shape) != (self.num_p,):
+            raise ValueError(f"state dimensions {tuple(u.shape)}/{tuple(p.shape)} do not match "
+                             f"operator {self.u_shape}/{(self.num_p,)}")
+
+    def _dev(self, a):
+        torch = _torch()
+        if isinstance(a, np.ndarray):
+            return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.device)
+        if a.dtype != torch.float64 or a.device != self.device or not a.is_contiguous():
+            raise ValueError("device arrays must be contiguous float64 on the operator's device")
+        return a
+
+    # -- operator application ---------------------------------------------------
+
+    def apply(self, state, out: State | None = None) -> State:
+        """Residual of the coupling operator acting on [u, p] (operator.py:331-362)."""
+        self._check(state)
+        self.counters.operator_applies += 1
+        host = isinstance(state.u, np.ndarray)
+        u, p = self._dev(state.u), self._dev(state.p)
+        torch = _torch()
+        ou = torch.empty_like(u) if out is None else self._dev(out.u)
+        op = torch.empty_like(p) if out is None else self._dev(out.p)
+        _lib.check(self._lib.fk_mix_apply(self._h, u.data_ptr(), p.data_ptr(), ou.data_ptr(),
+                                          op.data_ptr()))
+        if host:
+            return State(ou.cpu().numpy(), op.cpu().numpy())
+        return State(ou, op) if out is None else out
+
+    __call__ = apply
+
+    def apply_fused_normal(self, x_u):
+        """Velocity -> assembled pressure -> velocity (operator.py:364-387)."""
+        host = isinstance(x_u, np.ndarray)
+        if tuple(x_u.shape) != self.u_shape:
+            raise ValueError(f"velocity dimensions {tuple(x_u.shape)} do not match {self.u_shape}")
+        u = self._dev(x_u)
+        out = _torch().empty_like(u)
+        _lib.check(self._lib.fk_mix_fused_normal(self._h, u.data_ptr(), out.data_ptr()))
+        return out.cpu().numpy() if host else out
+
+    def apply_mass_inverse(self, residual) -> State:
+        """u / lump_u, p / lump_p (operator.py:391-397)."""
+        self._check(residual)
+        host = isinstance(residual.u, np.ndarray)
+        ru, rp = self._dev(residual.u), self._dev(residual.p)
+        u, p = _torch().empty_like(ru), _torch().empty_like(rp)
+        _lib.check(self._lib.fk_mix_mass_inverse(self._h, ru.data_ptr(), rp.data_ptr(),
+                                                 u.data_ptr(), p.data_ptr()))
+        return State(u.cpu().numpy(), p.cpu().numpy()) if host else State(u, p)
+
+    def lumped(self):
+        """(lump_u (nel, du^3), lump_p (num_p)) as NumPy arrays (QuadData.lump_u / lump_p)."""
+        torch = _torch()
+        lu = torch.empty((self.num_elements, self.num_dofs_u_local), dtype=torch.float64,
+                         device=self.device)
+        lp = torch.empty(self.num_p, dtype=torch.float64, device=self.device)
+        _lib.check(self._lib.fk_mix_lumped(self._h, lu.data_ptr(), lp.data_ptr()))
+        return lu.cpu().numpy(), lp.cpu().numpy()
+
+    def restriction_ids(self) -> np.ndarray:
+        d3 = (self.order_p + 1) ** 3
+        out = np.empty((self.num_elements, d3), dtype=np.int64)
+        _lib.check(self._lib.fk_mix_restriction(self._h, out.ctypes.data_as(
+            ctypes.POINTER(ctypes.c_int64))))
+        return out
+
+    def rk4(self, state, dt: float, steps: int = 1) -> State:
+        """``steps`` RK4 steps (rk4_step, operator.py:506-531, no forcing) on the
+        device, four fused applies per step; returns the new state."""
+        self._check(state)
+        if not dt > 0:
+            raise ValueError(f"dt must be positive, got {dt}")
+        host = isinstance(state.u, np.ndarray)
+        u, p = self._dev(state.u).clone(), self._dev(state.p).clone()
+        self.counters.operator_applies += 4 * int(steps)
+        _lib.check(self._lib.fk_mix_rk4(self._h, u.data_ptr(), p.data_ptr(), float(dt), int(steps)))
+        torch = _torch()
+        if not (bool(torch.isfinite(u).all()) and bool(torch.isfinite(p).all())):
+            raise DivergenceError(f"non-finite state after {steps} step(s)")
+        return State(u.cpu().numpy(), p.cpu().numpy()) if host else State(u, p)
+
+    def time_apply(self, state: State, out: State, reps: int) -> tuple[float, float]:
+        fa, fk = ctypes.c_double(), ctypes.c_double()
+        _lib.check(self._lib.fk_mix_time_apply(self._h, state.u.data_ptr(), state.p.data_ptr(),
+                                               out.u.data_ptr(), out.p.data_ptr(), int(reps),
+                                               ctypes.byref(fa), ctypes.byref(fk)))
+        return fa.value, fk.value
+
+    # -- algorithmic work (bench roofline) ---------------------------------------
+
+    @property
+    def bytes_per_apply(self) -> int:
+        """u read + out_u write (48 du^3 per element), p read + out_p write
+        (16 per H1 dof), dmat (72 q^3), int32 map (4 dp^3) per element."""
+        du3, dp3, q3 = (self.order_u + 1) ** 3, (self.order_p + 1) ** 3, self.num_quad_1d ** 3
+        return self.num_elements * (48 * du3 + 72 * q3 + 4 * dp3) + 16 * self.num_p
+
+    def gather_ids(self) -> np.ndarray:
+        return h1_gather_ids(self.mesh.nx, self.mesh.ny, self.mesh.nz, self.order_p + 1)
+
+
+def rk4_step(state, dt: float, op: MixedOperator, forcing=None, t: float = 0.0,
+             step_index: int = 0) -> State:
+    """Classical RK4 step (operator.py:506-531) on the device; forcing is not
+    supported on the B200 path."""
+    if forcing is not None:
+        raise NotImplementedError("forcing is not supported by the device RK4 driver")
+    if dt <= 0:
+        raise ValueError(f"dt must be positive, got {dt}")
+    try:
+        return op.rk4(state, dt, 1)
+    except DivergenceError as ex:
+        raise DivergenceError(f"non-finite state after step {step_index}") from ex
