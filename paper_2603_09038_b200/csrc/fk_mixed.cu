@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -22,7 +23,7 @@ using fk::MixArgs;
 constexpr int kMixMaxP = 8;
 
 struct MixKernel {
-  int dp = 0, du = 0, q = 0, E = 0, T = 0, ps = 0, gs = 0;
+  int dp = 0, du = 0, q = 0, cfg = 0, E = 0, T = 0, ps = 0, gs = 0;
   size_t smem = 0;
   const void* f_both = nullptr;
   const void* f_tau = nullptr;
@@ -35,18 +36,24 @@ enum { MIX_BOTH = 0, MIX_TAU = 1, MIX_VB = 2 };
 
 constexpr int round32(int n) { return (n + 31) / 32 * 32; }
 
-template <int DP, int DU, int Q>
+// Launch geometries: E ~ EB / NMAX elements per CTA (NMAX = lines of the
+// widest stage), one thread per line of the widest stage (measured: fewer
+// threads, e.g. one per stage-C line, is slower at every order)
+template <int DP, int DU, int Q, int CFG>
 struct MixGeom {
   static constexpr int NA = DP * DP + 3 * DU * DU, NB = Q * DP + 3 * Q * DU, NC = 2 * Q * Q;
   static constexpr int NMAX = NB > NA ? (NB > NC ? NB : NC) : (NA > NC ? NA : NC);
-  static constexpr int E = 192 / NMAX > 0 ? 192 / NMAX : 1;
-  static constexpr int T = round32(E * NMAX) > 384 ? 384 : round32(E * NMAX);
+  static constexpr int EB = CFG == 1 ? 384 : CFG == 2 ? 96 : CFG == 3 ? 288 : 192;
+  static constexpr int E = EB / NMAX > 0 ? EB / NMAX : 1;
+  static constexpr int TL = E * NMAX;  // one thread per line of the widest stage
+  static constexpr int T = round32(TL) > 384 ? 384 : round32(TL);
 };
+constexpr int kMixCfgs = 4;
 
-template <int DP, int DU, int Q>
+template <int DP, int DU, int Q, int CFG>
 void mix_launch(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
                 const MixArgs& a, int mode, int blocks, cudaStream_t s) {
-  using G = MixGeom<DP, DU, Q>;
+  using G = MixGeom<DP, DU, Q, CFG>;
   fk::MixTables<DP, DU, Q> tb;
   tb.fill(Bp, Gp, Bu);
   const size_t smem = fk::MixSmem<DP, DU, Q, G::E>::BYTES;
@@ -58,15 +65,16 @@ void mix_launch(const MixKernel&, const double* Bp, const double* Gp, const doub
     fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true><<<blocks, G::T, smem, s>>>(tb, a);
 }
 
-template <int P>
+template <int P, int CFG>
 MixKernel mix_entry() {
   constexpr int DP = P + 1, DU = P, Q = P + 1;
-  using G = MixGeom<DP, DU, Q>;
+  using G = MixGeom<DP, DU, Q, CFG>;
   using L = fk::MixLayout<DP, DU, Q>;
   MixKernel k;
   k.dp = DP;
   k.du = DU;
   k.q = Q;
+  k.cfg = CFG;
   k.E = G::E;
   k.T = G::T;
   k.ps = L::PS;
@@ -75,16 +83,36 @@ MixKernel mix_entry() {
   k.f_both = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true>);
   k.f_tau = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false>);
   k.f_vb = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true>);
-  k.launch = &mix_launch<DP, DU, Q>;
+  k.launch = &mix_launch<DP, DU, Q, CFG>;
   return k;
 }
 
+template <int P>
+void mix_add(std::vector<MixKernel>& v) {
+  v.push_back(mix_entry<P, 0>());
+  v.push_back(mix_entry<P, 1>());
+  v.push_back(mix_entry<P, 2>());
+  v.push_back(mix_entry<P, 3>());
+}
+
 const std::vector<MixKernel>& mix_registry() {
-  static const std::vector<MixKernel> reg = {mix_entry<2>(), mix_entry<3>(), mix_entry<4>(),
-                                             mix_entry<5>(), mix_entry<6>(), mix_entry<7>(),
-                                             mix_entry<8>()};
+  static const std::vector<MixKernel> reg = [] {
+    std::vector<MixKernel> v;
+    mix_add<2>(v);
+    mix_add<3>(v);
+    mix_add<4>(v);
+    mix_add<5>(v);
+    mix_add<6>(v);
+    mix_add<7>(v);
+    mix_add<8>(v);
+    return v;
+  }();
   return reg;
 }
+
+// default geometry per order_p (index = order_p): fastest in the bench --mixed
+// sweep (tools/gpu_mixsweep.sh, profiles/r01_mixed_sweep_v2.jsonl)
+const int kMixAutoCfg[9] = {0, 0, 1, 3, 2, 3, 0, 0, 0};
 
 int grid_for(int64_t n, int threads, int num_sms) {
   int64_t b = (n + threads - 1) / threads;
@@ -306,8 +334,14 @@ int fk_mix_create(fk_mix** out, const fk_mix_desc* d) {
     m->rho[e] = r;
     m->kinv[e] = 1.0 / k;
   }
+  int cfg = kMixAutoCfg[d->order_p];
+  if (const char* c = std::getenv("FK_MIX_CFG")) cfg = std::atoi(c);
+  if (cfg < 0 || cfg >= kMixCfgs) {
+    delete m;
+    return fk_fail(FK_EUNSUPPORTED, "no mixed launch config %d", cfg);
+  }
   for (const auto& k : mix_registry())
-    if (k.dp == m->dp && k.du == m->du && k.q == m->q) m->kern = &k;
+    if (k.dp == m->dp && k.du == m->du && k.q == m->q && k.cfg == cfg) m->kern = &k;
   if (m->kern == nullptr) {
     delete m;
     return fk_fail(FK_EUNSUPPORTED, "no kernel for order_p=%d", d->order_p);
