@@ -35,6 +35,9 @@ struct MixKernel {
 enum { MIX_BOTH = 0, MIX_TAU = 1, MIX_VB = 2 };
 
 constexpr int round32(int n) { return (n + 31) / 32 * 32; }
+constexpr int cmax5(int a, int b, int c, int d, int e) {
+  return fk::cmax(fk::cmax(a, b), fk::cmax(c, fk::cmax(d, e)));
+}
 
 // Launch geometries: E ~ EB / NMAX elements per CTA (NMAX = lines of the
 // widest stage), one thread per line of the widest stage (measured: fewer
@@ -45,7 +48,14 @@ struct MixGeom {
   static constexpr int NMAX = NB > NA ? (NB > NC ? NB : NC) : (NA > NC ? NA : NC);
   static constexpr int EB = CFG == 1 ? 384 : CFG == 2 ? 96 : CFG == 3 ? 288 : 192;
   static constexpr int E = EB / NMAX > 0 ? EB / NMAX : 1;
-  static constexpr int TL = E * NMAX;  // one thread per line of the widest stage
+  // one thread per line of the widest stage, the two blocks' lines of a stage
+  // laid out warp-aligned (mix_pipe.cuh lines())
+  static constexpr int PA_ = round32(E * DP * DP) + E * 3 * DU * DU;
+  static constexpr int PB_ = round32(E * Q * DP) + E * 3 * Q * DU;
+  static constexpr int PC_ = round32(E * Q * Q) + E * Q * Q;
+  static constexpr int PD_ = round32(E * 3 * Q * DU) + E * Q * DP;
+  static constexpr int PE_ = round32(E * 3 * DU * DU) + E * DP * DP;
+  static constexpr int TL = cmax5(PA_, PB_, PC_, PD_, PE_);
   static constexpr int T = round32(TL) > 384 ? 384 : round32(TL);
 };
 constexpr int kMixCfgs = 4;
@@ -111,8 +121,8 @@ const std::vector<MixKernel>& mix_registry() {
 }
 
 // default geometry per order_p (index = order_p): fastest in the bench --mixed
-// sweep (tools/gpu_mixsweep.sh, profiles/r01_mixed_sweep_v2.jsonl)
-const int kMixAutoCfg[9] = {0, 0, 1, 3, 2, 3, 0, 0, 0};
+// sweep (tools/gpu_mixsweep.sh, profiles/r01_mixed_sweep_v3_warp_aligned.jsonl)
+const int kMixAutoCfg[9] = {0, 0, 0, 3, 2, 2, 0, 0, 0};
 
 int grid_for(int64_t n, int threads, int num_sms) {
   int64_t b = (n + threads - 1) / threads;

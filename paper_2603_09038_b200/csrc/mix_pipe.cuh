@@ -206,10 +206,21 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
     ph_g ^= 1u << slot;
   };
   // element-major thread -> (e, line) loop over a stage's lines
-  auto lines = [&](int ne, int nl, auto f) {
-    for (int t = threadIdx.x; t < E * nl; t += T) {
-      const int e = t / nl, l = t - e * nl;
-      if (e < ne) f(e, l);
+  // f(e, l) over a stage's two line groups: l in [0, n1) (first block) and
+  // [n1, n1 + n2) (second block).  The groups are laid out phase-major and
+  // the second starts on a warp boundary, so no warp runs both code paths.
+  auto lines = [&](int ne, int n1, int n2, auto f) {
+    const int pad = (E * n1 + 31) & ~31;
+    for (int t = threadIdx.x; t < pad + E * n2; t += T) {
+      if (t < pad) {
+        if (t < E * n1) {
+          const int e = t / n1, l = t - e * n1;
+          if (e < ne) f(e, l);
+        }
+      } else {
+        const int m = t - pad, e = m / n2, l = n1 + (m - e * n2);
+        if (e < ne) f(e, l);
+      }
     }
   };
   constexpr int NAP = TAU ? DP * DP : 0, NAU = VB ? 3 * DU * DU : 0;
@@ -244,7 +255,7 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
       }
     }
     // ---- stage A: x contraction
-    lines(ne, NAP + NAU, [&](int e, int l) {
+    lines(ne, NAP, NAU, [&](int e, int l) {
       if (TAU && l < NAP) {
         const int j = l % DP, k = l / DP;
         double xr[DP], o[Q];
@@ -268,7 +279,7 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
     });
     __syncthreads();
     // ---- stage B: y contraction
-    lines(ne, NBP + NBU, [&](int e, int l) {
+    lines(ne, NBP, NBU, [&](int e, int l) {
       if (TAU && l < NBP) {
         const int a = l / DP, k = l % DP;
         double bx[DP], gx[DP], c[Q];
@@ -300,7 +311,7 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
     // ---- stage C: z + D + z^T (D read once for both blocks)
     mbar_wait(bar_d, ph_d);
     ph_d ^= 1u;
-    lines(ne, NCP + NCU, [&](int e, int l) {
+    lines(ne, NCP, NCU, [&](int e, int l) {
       const bool pph = TAU && l < NCP;
       const int m = pph ? l : l - NCP;
       const int a = m % Q, b2 = m / Q;
@@ -369,7 +380,7 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
       issue_d(nb);
     }
     // ---- stage D: y^T
-    lines(ne, NDU + NDP, [&](int e, int l) {
+    lines(ne, NDU, NDP, [&](int e, int l) {
       if (TAU && l < NDU) {
         const int r = l / (Q * DU), ak = l - r * (Q * DU), a = ak % Q, k = ak / Q;
         double v[Q], o[DU];
@@ -400,7 +411,7 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
     // ---- stage E: x^T, outputs
     const int* g = gs + gslot * E * GS;
     constexpr int NEU = TAU ? 3 * DU * DU : 0, NEP = VB ? DP * DP : 0;
-    lines(ne, NEU + NEP, [&](int e, int l) {
+    lines(ne, NEU, NEP, [&](int e, int l) {
       if (TAU && l < NEU) {
         const int r = l / (DU * DU), jk = l - r * (DU * DU), j = jk % DU, k = jk / DU;
         double v[Q], o[DU];
