@@ -545,7 +545,7 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
     FK_CUDA(cudaStreamCreateWithFlags(&op->d2h, cudaStreamNonBlocking));
     for (auto& e : op->chunk_ev) FK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  int K = std::min(nzl, 8);
+  int K = std::min(nzl, 8);  // tools/pcie_probe.py: 8 ramped chunks measured best
   if (const char* c = std::getenv("FK_HOST_CHUNKS")) K = std::max(1, std::min({nzl, std::atoi(c), 15}));
   const int64_t P = op->npx * op->npy, nxy = (int64_t)op->desc.nx * op->desc.ny;
   const int p = op->p;
@@ -553,8 +553,20 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
   FK_CUDA(cudaStreamWaitEvent(op->h2d, op->chunk_ev[30], 0));
   FK_CUDA(cudaMemsetAsync(op->stage_y, 0, bytes, op->stream));
   int64_t x_done = 0, y_done = 0;
+  // chunk boundaries on a smoothstep ramp: small first and last chunks shorten
+  // the pipeline fill (H2D before the first compute) and drain (compute + D2H
+  // after the last H2D); FK_HOST_RAMP=0 gives uniform chunks
+  const char* ramp_env = std::getenv("FK_HOST_RAMP");
+  const bool ramp = !(ramp_env && ramp_env[0] == '0');
+  auto zb = [&](int c) {
+    if (c <= 0) return 0;
+    if (c >= K) return nzl;
+    const double t = (double)c / K, f = ramp ? t * t * (3.0 - 2.0 * t) : t;
+    return std::min(nzl, std::max(1, (int)std::lround(f * nzl)));
+  };
   for (int c = 0; c < K; ++c) {
-    const int z0 = (int)((int64_t)nzl * c / K), z1 = (int)((int64_t)nzl * (c + 1) / K);
+    const int z0 = zb(c), z1 = zb(c + 1);
+    if (z1 <= z0) continue;
     const int64_t x_hi = (int64_t)z1 * p + 1;
     FK_CUDA(cudaMemcpyAsync(op->stage_x + x_done * P, xh + x_done * P,
                             sizeof(double) * (x_hi - x_done) * P, cudaMemcpyHostToDevice, op->h2d));
@@ -565,7 +577,7 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
                         op->stream));
     FK_CUDA(cudaEventRecord(op->chunk_ev[2 * c + 1], op->stream));
     FK_CUDA(cudaStreamWaitEvent(op->d2h, op->chunk_ev[2 * c + 1], 0));
-    const int64_t y_hi = (c == K - 1) ? op->npz_local : (int64_t)z1 * p;
+    const int64_t y_hi = (z1 == nzl) ? op->npz_local : (int64_t)z1 * p;
     FK_CUDA(cudaMemcpyAsync(yh + y_done * P, op->stage_y + y_done * P,
                             sizeof(double) * (y_hi - y_done) * P, cudaMemcpyDeviceToHost, op->d2h));
     y_done = y_hi;

@@ -46,15 +46,17 @@ def main():
     xh = torch.empty(op.num_dofs, dtype=torch.float64, pin_memory=True).numpy()
     yh = torch.empty(op.num_dofs, dtype=torch.float64, pin_memory=True).numpy()
     xh[:] = np.random.default_rng(0).standard_normal(op.num_dofs)
-    for k in (1, 2, 4, 8, 12, 15):
-        os.environ["FK_HOST_CHUNKS"] = str(k)
-        for _ in range(3):
-            op.apply_host(xh, yh)
-        t0 = time.perf_counter()
-        for _ in range(20):
-            op.apply_host(xh, yh)
-        dt = (time.perf_counter() - t0) / 20
-        res[f"apply_host_K{k}"] = {"ms": dt * 1e3, "GDOF/s": op.num_dofs / dt / 1e9}
+    for ramp in ("0", "1"):
+        os.environ["FK_HOST_RAMP"] = ramp
+        for k in (4, 8, 12, 15):
+            os.environ["FK_HOST_CHUNKS"] = str(k)
+            for _ in range(3):
+                op.apply_host(xh, yh)
+            t0 = time.perf_counter()
+            for _ in range(30):
+                op.apply_host(xh, yh)
+            dt = (time.perf_counter() - t0) / 30
+            res[f"apply_host_K{k}_ramp{ramp}"] = {"ms": dt * 1e3, "GDOF/s": op.num_dofs / dt / 1e9}
     print(json.dumps(res, indent=1))
 
 
