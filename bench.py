@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--p", type=int, default=None, help="order (default 4; 6 for --cg strong)")
     ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--n", type=int, default=None, help="elements per direction (per-rank slab is n^3)")
-    ap.add_argument("--variant", default="auto", choices=["auto", "dfma", "dmma", "eo"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "dfma", "dmma", "eo", "mf"])
     ap.add_argument("--sweep", default=None, help="also run the p=1..8 DFMA/DMMA sweep, JSON lines to FILE")
     ap.add_argument("--sweep-cfgs", default=None,
                     help="restrict the sweep to these geometries, e.g. 'eo0,eo9,dfma2'")
@@ -336,8 +336,9 @@ def run_ours(a):
             except Exception as ex:  # reported, never fatal for the GPU number
                 cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                        "sample": f"failed: {ex}"}
-        work = (f"BP3 PA diffusion apply p={p} q={q}" if a.kind == "diffusion"
-                else f"BP1 PA mass apply p={p} q={q}")
+        strat = "MF (matrix-free)" if op.variant == "mf" else "PA"
+        work = (f"BP3 {strat} diffusion apply p={p} q={q}" if a.kind == "diffusion"
+                else f"BP1 {strat} mass apply p={p} q={q}")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -348,8 +349,8 @@ def run_ours(a):
                        "elements_per_gpu": n ** 3, "dofs_per_gpu": op.num_dofs,
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                        "variant": op.variant,
-                       "l2": (f"inputs larger than L2 (PA data {op.info.pa_bytes / 1e9:.2f} GB "
-                              "per apply, no flush needed)" if op.bytes_per_apply > 126e6 else
+                       "l2": ((f"inputs larger than L2 ({op.bytes_per_apply / 1e9:.2f} GB moved "
+                               "per apply, no flush needed)") if op.bytes_per_apply > 126e6 else
                               "small config: L2-resident between steps (not a bandwidth number)"),
                        "launch": {"elems_per_block": op.info.elems_per_block,
                                   "threads": op.info.threads_per_block, "blocks": op.info.blocks}},
@@ -511,7 +512,7 @@ def run_sweep(a, peak):
 
     out = []
     cfgs = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(3)]
-            + [("eo", c) for c in range(19)])
+            + [("eo", c) for c in range(19)] + [("mf", c) for c in range(8)])
     if a.sweep_cfgs:
         want = set(a.sweep_cfgs.split(","))
         cfgs = [vc for vc in cfgs if f"{vc[0]}{vc[1]}" in want]

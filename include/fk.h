@@ -48,7 +48,10 @@ extern "C" {
 #define FK_VARIANT_DMMA 2   /* warp mma.sync.m8n8k4 f64 tiles (DMMA.8x8x4)           */
 #define FK_VARIANT_EO 3     /* FP64 FMA with even-odd folding of the symmetric 1D tables
                                (half the multiply-adds; symmetric bases only)         */
-#define FK_VARIANT_LAST FK_VARIANT_EO
+#define FK_VARIANT_MF 4     /* matrix-free (the reference's MF strategy, operator.py:280-286):
+                               even-odd FMA kernel that recomputes D = w|J|J^-1J^-T of the
+                               axis-aligned box in stage C instead of reading PA data */
+#define FK_VARIANT_LAST FK_VARIANT_MF
 
 typedef struct fk_op fk_op;
 typedef struct fk_comm fk_comm;

@@ -28,9 +28,10 @@ FK_VARIANT_DFMA = 1
 FK_VARIANT_DMMA = 2
 
 FK_VARIANT_EO = 3
+FK_VARIANT_MF = 4
 
 VARIANTS = {"auto": FK_VARIANT_AUTO, "dfma": FK_VARIANT_DFMA, "dmma": FK_VARIANT_DMMA,
-            "eo": FK_VARIANT_EO}
+            "eo": FK_VARIANT_EO, "mf": FK_VARIANT_MF}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 
 #: every symbol include/fk.h declares (checked by tests/test_cabi.py)

@@ -71,6 +71,14 @@ int auto_variant(int nc, int p, int q) {
   return nc == 3 ? kAutoVar3[p] : kAutoVar1[p];
 }
 
+// matrix-free geometry per order (best of profiles/r01_sweep_v14_mf.jsonl)
+const int kAutoCfgMF3[9] = {0, 7, 3, 5, 5, 5, 6, 5, 6};
+const int kAutoCfgMF1[9] = {0, 3, 3, 3, 4, 5, 4, 4, 4};
+int auto_cfg_mf(int nc, int p) {
+  if (p < 1 || p > 8) return 0;
+  return nc == 3 ? kAutoCfgMF3[p] : kAutoCfgMF1[p];
+}
+
 int auto_cfg(int nc, int p) {
   if (p < 1 || p > 8) return 0;
   return nc == 3 ? kAutoCfg3[p] : kAutoCfg1[p];
@@ -84,6 +92,9 @@ fk::OpView view(const fk_op* op) {
   v.pa = op->pa;
   v.ebits = op->ebits;
   v.nel = (int)op->nel;
+  v.w = op->w;
+  v.detj = op->desc.jac_det;
+  for (int s = 0; s < 3; ++s) v.jinv[s] = op->jinv[s];
   return v;
 }
 
@@ -104,18 +115,19 @@ bool tables_symmetric(const fk_op* op) {
 
 int select_kernel(fk_op* op, int variant) {
   int v = variant == FK_VARIANT_AUTO ? auto_variant(op->nc, op->p, op->q) : variant;
-  if (v == FK_VARIANT_EO && !tables_symmetric(op)) {
+  if ((v == FK_VARIANT_EO || v == FK_VARIANT_MF) && !tables_symmetric(op)) {
     if (variant != FK_VARIANT_AUTO)
-      return fail(FK_EUNSUPPORTED, "even-odd variant needs symmetric basis tables");
+      return fail(FK_EUNSUPPORTED, "even-odd / matrix-free variants need symmetric basis tables");
     v = FK_VARIANT_DFMA;
   }
   const fk::KernelEntry* k = nullptr;
   if (op->cfg >= 0) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, op->cfg);
   else if (variant == FK_VARIANT_AUTO) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, auto_cfg(op->nc, op->p));
+  else if (variant == FK_VARIANT_MF) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, auto_cfg_mf(op->nc, op->p));
   if (k == nullptr) k = fk::find_kernel(op->nc, op->d, op->q, v);
   if (k == nullptr)
     return fail(FK_EUNSUPPORTED, "no %s kernel compiled for kind=%d p=%d q=%d",
-                v == FK_VARIANT_DMMA ? "DMMA" : v == FK_VARIANT_EO ? "even-odd" : "DFMA",
+                v == FK_VARIANT_DMMA ? "DMMA" : v == FK_VARIANT_EO ? "even-odd" : v == FK_VARIANT_MF ? "matrix-free" : "DFMA",
                 op->desc.kind, op->p, op->q);
   {
     int max_smem = 0;

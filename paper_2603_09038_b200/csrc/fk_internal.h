@@ -32,6 +32,9 @@ struct OpView {
   const double* pa;
   const uint32_t* ebits;  // per-element Dirichlet bits (nullptr: none)
   int nel;
+  const double* w;  // host quadrature weights (q), |J| and 1/jac_diag: MF kernels
+  double detj;
+  double jinv[3];
 };
 
 // Host mirror of GlobalLayout (pa_common.cuh): padded per-element strides.

@@ -39,6 +39,11 @@ struct __align__(16) FoldTables {
   static constexpr int TB = 0, TG = FQD::SIZE, TBT = 2 * FQD::SIZE, TGT = 2 * FQD::SIZE + FDQ::SIZE;
   static constexpr int SZ = 2 * FQD::SIZE + 2 * FDQ::SIZE;
   double t[2][SZ];  // two copies (ping-pong by batch parity, see pa_dfma.cuh)
+  // matrix-free (MF) factors: 1D quadrature weights, |J| and jinv_s^2
+  // (operator.py:137-144, 280-286: the reference's MF recomputes the diagonal
+  // w|J|J^-1 of the axis-aligned box per element instead of reading dmat)
+  double mfw[Q + (Q & 1)];
+  double mfc[4];  // detJ, jinv_0^2, jinv_1^2, jinv_2^2
 };
 
 // host: fold N (NO x NI, row-major) with symmetry sign S into dst (Fold layout)
@@ -230,6 +235,12 @@ struct DfmaEoBody {
     }
   }
 
+  static void fill_mf(Tab& tb, const double* w, double detj, const double* jinv) {
+    for (int a = 0; a < Q; ++a) tb.mfw[a] = w[a];
+    tb.mfc[0] = detj;
+    for (int s = 0; s < 3; ++s) tb.mfc[1 + s] = jinv[s] * jinv[s];
+  }
+
   __device__ static void init(const Tab&, double*) {}
 
   // run f(e, p1, p2) over the stage's lines of the batch's ne elements
@@ -297,7 +308,10 @@ struct DfmaEoBody {
     });
   }
 
-  // T2 (a, b, k) + D -> W (a, b, k): thread per line (a, b); W region sw
+  // T2 (a, b, k) + D -> W (a, b, k): thread per line (a, b); W region sw.
+  // MF: D computed from the 1D weights and the element Jacobian, in the PA
+  // setup's operation order (fk_setup.cuh pa_data_kernel), so bit-identical.
+  template <bool MF = false>
   __device__ __forceinline__ static void stage_c(const Tab& tb, int it, const double* s0,
                                                  const double* db, double* sw, int ne, double*) {
     const double* tab = tb.t[PP ? (it & 1) : 0];
@@ -317,7 +331,8 @@ struct DfmaEoBody {
         for (int k = 0; k < D; ++k) tin[s][k] = s0[LT2::at(e, s, a, b, k)];
       if constexpr (IP) __syncthreads();  // every T2 line is in registers: W may overwrite it
       if (!act) continue;
-      const double* pe = db + e * G::PS + a + Q * b;
+      const double* pe = MF ? nullptr : db + e * G::PS + a + Q * b;
+      const double wab = MF ? tb.mfw[b] * tb.mfw[a] : 0.0;
       if constexpr (NC == 3) {
         double g0[Q], g1[Q], g2[Q];
         contract_eo<D, Q, +1>(tab + Tab::TB, tin[0], g0);
@@ -325,13 +340,20 @@ struct DfmaEoBody {
         contract_eo<D, Q, -1>(tab + Tab::TG, tin[NC - 1], g2);
 #pragma unroll
         for (int c = 0; c < Q; ++c) {
-          const double* pc = pe + c * Q * Q;
-          const double d00 = pc[0 * Q3], d01 = pc[1 * Q3], d02 = pc[2 * Q3];
-          const double d11 = pc[3 * Q3], d12 = pc[4 * Q3], d22 = pc[5 * Q3];
           const double a0 = g0[c], a1 = g1[c], a2 = g2[c];
-          g0[c] = fma(d02, a2, fma(d01, a1, d00 * a0));
-          g1[c] = fma(d12, a2, fma(d11, a1, d01 * a0));
-          g2[c] = fma(d22, a2, fma(d12, a1, d02 * a0));
+          if constexpr (MF) {
+            const double wdet = (tb.mfw[c] * wab) * tb.mfc[0];
+            g0[c] = (wdet * tb.mfc[1]) * a0;
+            g1[c] = (wdet * tb.mfc[2]) * a1;
+            g2[c] = (wdet * tb.mfc[3]) * a2;
+          } else {
+            const double* pc = pe + c * Q * Q;
+            const double d00 = pc[0 * Q3], d01 = pc[1 * Q3], d02 = pc[2 * Q3];
+            const double d11 = pc[3 * Q3], d12 = pc[4 * Q3], d22 = pc[5 * Q3];
+            g0[c] = fma(d02, a2, fma(d01, a1, d00 * a0));
+            g1[c] = fma(d12, a2, fma(d11, a1, d01 * a0));
+            g2[c] = fma(d22, a2, fma(d12, a1, d02 * a0));
+          }
         }
         double w[D];
         contract_eo<Q, D, +1>(tab + Tab::TBT, g0, w);
@@ -347,7 +369,7 @@ struct DfmaEoBody {
         double g[Q], w[D];
         contract_eo<D, Q, +1>(tab + Tab::TB, tin[0], g);
 #pragma unroll
-        for (int c = 0; c < Q; ++c) g[c] *= pe[c * Q * Q];
+        for (int c = 0; c < Q; ++c) g[c] *= MF ? (tb.mfw[c] * wab) * tb.mfc[0] : pe[c * Q * Q];
         contract_eo<Q, D, +1>(tab + Tab::TBT, g, w);
 #pragma unroll
         for (int k = 0; k < D; ++k) sw[LW::at(e, 0, a, b, k)] = w[k];

@@ -26,12 +26,13 @@ constexpr int round32(int n) { return ((n + 31) / 32) * 32; }
 // stage C (q^2 lines per element) is the heaviest: E*q^2 lines ~ 288
 constexpr int base_E(int Q) { return (288 / (Q * Q)) > 0 ? (288 / (Q * Q)) : 1; }
 
-template <int D, int Q, int NC, class Body, bool PERSIST, bool DG>
+template <int D, int Q, int NC, class Body, bool PERSIST, bool DG, bool MF = false>
 void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
   typename Body::Tab tb;
   Body::fill(tb, v.B, v.G);
-  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG>
-      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body, DG>::BYTES, s>>>(
+  if constexpr (MF) Body::fill_mf(tb, v.w, v.detj, v.jinv);
+  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF>
+      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body, DG || MF>::BYTES, s>>>(
           tb, x, y, v.gids, v.pa, v.ebits, v.nel);
 }
 
@@ -43,7 +44,7 @@ void launch_diag(const OpView& v, double* diag, int64_t nel, int blocks, cudaStr
   diagonal_kernel<D, Q, NC><<<blocks, 128, 0, s>>>(tb, diag, v.gids, v.pa, nel);
 }
 
-template <int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false>
+template <int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false, bool MF = false>
 KernelEntry entry(int variant, int cfg) {
   KernelEntry k;
   k.nc = NC;
@@ -54,9 +55,9 @@ KernelEntry entry(int variant, int cfg) {
   k.E = Body::E;
   k.T = Body::T;
   k.persist = PERSIST;
-  k.smem = PipeSmem<D, Q, NC, Body, DG>::BYTES;
-  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG>);
-  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG>;
+  k.smem = PipeSmem<D, Q, NC, Body, DG || MF>::BYTES;
+  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF>);
+  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF>;
   k.diag = &launch_diag<D, Q, NC>;
   return k;
 }
@@ -111,6 +112,23 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, O2, true>(FK_VARIANT_EO, 0));
   add_tuned_eo<D, Q, NC, true>(out, 1);
   add_tuned_eo<D, Q, NC, false>(out, 10);
+  // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
+  using M2 = TunedEo<D, Q, NC, E2, false, true>;
+  using M1 = TunedEo<D, Q, NC, E1, false, true>;
+  using M2i = TunedEo<D, Q, NC, E2, true, true>;
+  using M0i = TunedEo<D, Q, NC, E0, true, true>;
+  using M2s = TunedEo<D, Q, NC, E2, false, false>;
+  using M1s = TunedEo<D, Q, NC, E1, false, false>;
+  using M2is = TunedEo<D, Q, NC, E2, true, false>;
+  using M0is = TunedEo<D, Q, NC, E0, true, false>;
+  out.push_back(entry<D, Q, NC, M2, true, false, true>(FK_VARIANT_MF, 0));
+  out.push_back(entry<D, Q, NC, M1, true, false, true>(FK_VARIANT_MF, 1));
+  out.push_back(entry<D, Q, NC, M2i, true, false, true>(FK_VARIANT_MF, 2));
+  out.push_back(entry<D, Q, NC, M0i, true, false, true>(FK_VARIANT_MF, 3));
+  out.push_back(entry<D, Q, NC, M2s, true, false, true>(FK_VARIANT_MF, 4));
+  out.push_back(entry<D, Q, NC, M1s, true, false, true>(FK_VARIANT_MF, 5));
+  out.push_back(entry<D, Q, NC, M2is, true, false, true>(FK_VARIANT_MF, 6));
+  out.push_back(entry<D, Q, NC, M0is, true, false, true>(FK_VARIANT_MF, 7));
 }
 
 }  // namespace

@@ -73,7 +73,9 @@ struct PipeSmem {
 // DG (high orders, where E*48q^3 bytes of smem would cap occupancy): stage C
 // reads D straight from global memory; the next batch's D range is pulled
 // toward L2 with cp.async.bulk.prefetch.L2 instead of copied into smem.
-template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false>
+// MF (matrix-free, even-odd bodies only): no PA data at all — stage C
+// recomputes D from the 1D weights and the element Jacobian (Body::stage_c<true>).
+template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false, bool MF = false>
 __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ typename Body::Tab tb,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   constexpr int E = Body::E, T = Body::T;
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
-  using S = PipeSmem<D, Q, NC, Body, DG>;
+  using S = PipeSmem<D, Q, NC, Body, DG || MF>;
   using XA = XAddr<D, Q, NC, Body>;
   constexpr int D3 = L::D3, XS = S::XS, NG = S::NG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -126,6 +128,7 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     if (dirichlet) bulk_g2s(ms + slot * E * G::MS, ebits + (size_t)e0 * G::MS, mb, bar_g + slot);
   };
   auto issue_d = [&](int b) {
+    if constexpr (MF) return;
     const int e0 = b * E, ne = min(E, nel - e0);
     const uint32_t bytes = 8u * ne * G::PS;
     if constexpr (DG) {
@@ -197,7 +200,9 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     __syncthreads();
     Body::stage_b(tb, it, s1, s0, ne, ex);
     __syncthreads();
-    if constexpr (DG) {
+    if constexpr (MF) {
+      Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex);
+    } else if constexpr (DG) {
       Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex);
     } else {
       mbar_wait(bar_d, ph_d);

@@ -28,7 +28,10 @@ import numpy as np
 from . import _lib
 from .fem import Basis1D, Counters, ShapeError
 
-STRATEGIES = ("PA", "FusedPA")
+# PA / FusedPA: stored quadrature data (one fused kernel either way for a
+# single-block operator); MF / FusedMF: the factors recomputed in the kernel
+# (operator.py:16-19, 280-286) -> variant "mf"
+STRATEGIES = ("PA", "FusedPA", "MF", "FusedMF")
 KINDS = {"mass": _lib.FK_KIND_MASS, "diffusion": _lib.FK_KIND_DIFFUSION,
          "bp1": _lib.FK_KIND_MASS, "bp3": _lib.FK_KIND_DIFFUSION}
 
@@ -81,9 +84,10 @@ def flops_per_element(kind: str, d: int, q: int) -> int:
     return 2 * (4 * q * d ** 3 + 6 * q * q * d * d + 6 * q ** 3 * d) + 15 * q ** 3
 
 
-def bytes_per_apply(kind: str, ndof: int, nel: int, d: int, q: int) -> int:
-    """Algorithmic HBM bytes: x read, y write, D, int32 map."""
-    ncomp = 1 if KINDS[kind] == _lib.FK_KIND_MASS else 6
+def bytes_per_apply(kind: str, ndof: int, nel: int, d: int, q: int, mf: bool = False) -> int:
+    """Algorithmic HBM bytes: x read, y write, D (not for the
+    matrix-free variant), int32 map."""
+    ncomp = 0 if mf else (1 if KINDS[kind] == _lib.FK_KIND_MASS else 6)
     return 16 * ndof + 8 * ncomp * q ** 3 * nel + 4 * d ** 3 * nel
 
 
@@ -122,6 +126,10 @@ class PAOperator:
         lib = _lib.load()
         self.kind = "mass" if KINDS[kind] == _lib.FK_KIND_MASS else "diffusion"
         self.strategy = strategy
+        if strategy in ("MF", "FusedMF"):
+            if variant not in ("auto", "mf"):
+                raise ValueError(f"strategy {strategy!r} runs the matrix-free variant, got {variant!r}")
+            variant = "mf"
         self.mesh = mesh
         self.order = int(order)
         q = int(num_quad_1d) if num_quad_1d is not None else self.order + 2
@@ -188,8 +196,14 @@ class PAOperator:
         self.num_global_dofs = int(self.info.ndof_global)
         d, qq = self.order + 1, q
         self.flops_per_apply = flops_per_element(self.kind, d, qq) * self.num_elements
-        self.bytes_per_apply = bytes_per_apply(self.kind, self.num_dofs, self.num_elements, d, qq)
+        self._bytes = {mf: bytes_per_apply(self.kind, self.num_dofs, self.num_elements, d, qq, mf)
+                       for mf in (False, True)}
         self._ncomp = 1 if self.kind == "mass" else 6
+
+    @property
+    def bytes_per_apply(self) -> int:
+        """Algorithmic HBM bytes of one apply with the current variant."""
+        return self._bytes[self.variant == "mf"]
 
     # -- lifecycle ------------------------------------------------------------
 
@@ -221,8 +235,8 @@ class PAOperator:
 
     def set_config(self, variant: str, cfg: int) -> None:
         """Pick compiled launch geometry ``cfg`` of ``variant`` ("dfma"/"dmma")."""
-        if variant not in ("dfma", "dmma", "eo"):
-            raise ValueError(f"variant must be 'dfma', 'dmma' or 'eo', got {variant!r}")
+        if variant not in ("dfma", "dmma", "eo", "mf"):
+            raise ValueError(f"variant must be 'dfma', 'dmma', 'eo' or 'mf', got {variant!r}")
         _lib.check(self._lib.fk_op_set_config(self._h, _lib.VARIANTS[variant], int(cfg)))
         self.info = self._info()
 

@@ -34,7 +34,7 @@ def dev(x):
     return torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda")
 
 
-VARIANTS = ["dfma", "dmma", "eo"]
+VARIANTS = ["dfma", "dmma", "eo", "mf"]
 
 GOLDEN_CASES = (
     [("mass", (8, 8, 8), 2, None, (1.0, 1.0, 1.0), "bp1_8x8x8_p2")]
@@ -118,7 +118,7 @@ def test_apply_matches_oracle_all_orders(variant, kind, p, qoff):
 
 
 LAUNCH_CONFIGS = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(3)]
-                  + [("eo", c) for c in range(19)])
+                  + [("eo", c) for c in range(19)] + [("mf", c) for c in range(8)])
 
 
 @pytest.mark.parametrize("variant,cfg", LAUNCH_CONFIGS)
@@ -370,13 +370,30 @@ def test_shape_errors_and_counters():
     with pytest.raises(ValueError, match="do not match"):
         op.apply(np.zeros(3))
     with pytest.raises(ValueError):
-        make("diffusion", (2, 2, 2), 3, strategy="MF")
+        make("diffusion", (2, 2, 2), 3, strategy="scalar")
+    with pytest.raises(ValueError):  # MF runs the matrix-free variant only
+        make("diffusion", (2, 2, 2), 3, strategy="MF", variant="dmma")
     with pytest.raises(NotImplementedError):
         make("diffusion", (2, 2, 2), 3, 9)
     before = op.counters.operator_applies
     op.apply(op.zeros())
     assert op.counters.operator_applies == before + 1
     assert op.counters.flops == op.flops_per_apply * op.counters.operator_applies
+
+
+@pytest.mark.parametrize("strategy", ["MF", "FusedMF"])
+@pytest.mark.parametrize("kind", ["mass", "diffusion"])
+def test_matrix_free_strategy_matches_pa(strategy, kind):
+    """The reference's MF strategy (operator.py:280-286: factors recomputed per
+    element instead of read) through PAOperator(strategy=...) -> variant "mf"
+    with no PA data traffic; same operator as PA to rounding."""
+    for p, n in ((2, (5, 4, 3)), (4, (6, 5, 7)), (7, (3, 3, 2))):
+        P = bp.Problem(kind, *n, p)
+        x = np.random.default_rng(p).standard_normal(P.ndof)
+        op = make(kind, n, p, strategy=strategy)
+        assert op.variant == "mf"
+        assert op.bytes_per_apply == 16 * P.ndof + 4 * (p + 1) ** 3 * P.ids.shape[0]
+        assert normwise(op.apply(dev(x)).cpu().numpy(), P.apply(x)) <= PARITY_TOL
 
 
 def test_reference_objects_drop_in(golden):
