@@ -180,6 +180,8 @@ typedef struct fk_mix_desc {
   const double* bulk;          /* host per-element bulk modulus or NULL -> bulk_scalar */
   double rho_scalar, bulk_scalar;
   double coupling_scale;       /* BlockOperator coupling_scale */
+  int matrix_free;             /* 1: strategy FusedMF (dmat recomputed in the kernel,
+                                  operator.py:280-286); 0: FusedPA / PA */
   int device;
   void* stream;                /* cudaStream_t */
 } fk_mix_desc;

@@ -106,6 +106,7 @@ class FkMixDesc(ctypes.Structure):
         ("rho_scalar", ctypes.c_double),
         ("bulk_scalar", ctypes.c_double),
         ("coupling_scale", ctypes.c_double),
+        ("matrix_free", ctypes.c_int),
         ("device", ctypes.c_int),
         ("stream", ctypes.c_void_p),
     ]

@@ -24,15 +24,17 @@ constexpr int kMixMaxP = 8;
 
 struct MixKernel {
   int dp = 0, du = 0, q = 0, cfg = 0, E = 0, T = 0, ps = 0, gs = 0;
-  size_t smem = 0;
+  size_t smem = 0, smem_mf = 0;
   const void* f_both = nullptr;
   const void* f_tau = nullptr;
   const void* f_vb = nullptr;
+  const void* f_mf = nullptr;  // FusedMF apply (both blocks, no dmat traffic)
   void (*launch)(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
-                 const MixArgs& a, int mode, int blocks, cudaStream_t s) = nullptr;
+                 const double* w, double detj, const double* jinv, const MixArgs& a, int mode,
+                 int blocks, cudaStream_t s) = nullptr;
 };
 
-enum { MIX_BOTH = 0, MIX_TAU = 1, MIX_VB = 2 };
+enum { MIX_BOTH = 0, MIX_TAU = 1, MIX_VB = 2, MIX_BOTH_MF = 3 };
 
 constexpr int round32(int n) { return (n + 31) / 32 * 32; }
 constexpr int cmax5(int a, int b, int c, int d, int e) {
@@ -62,17 +64,22 @@ constexpr int kMixCfgs = 4;
 
 template <int DP, int DU, int Q, int CFG>
 void mix_launch(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
-                const MixArgs& a, int mode, int blocks, cudaStream_t s) {
+                const double* w, double detj, const double* jinv, const MixArgs& a, int mode,
+                int blocks, cudaStream_t s) {
   using G = MixGeom<DP, DU, Q, CFG>;
   fk::MixTables<DP, DU, Q> tb;
   tb.fill(Bp, Gp, Bu);
+  tb.fill_mf(w, detj, jinv);
   const size_t smem = fk::MixSmem<DP, DU, Q, G::E>::BYTES;
   if (mode == MIX_BOTH)
     fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true><<<blocks, G::T, smem, s>>>(tb, a);
   else if (mode == MIX_TAU)
     fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false><<<blocks, G::T, smem, s>>>(tb, a);
-  else
+  else if (mode == MIX_VB)
     fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true><<<blocks, G::T, smem, s>>>(tb, a);
+  else
+    fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true>
+        <<<blocks, G::T, fk::MixSmem<DP, DU, Q, G::E, true>::BYTES, s>>>(tb, a);
 }
 
 template <int P, int CFG>
@@ -90,9 +97,11 @@ MixKernel mix_entry() {
   k.ps = L::PS;
   k.gs = L::GS;
   k.smem = fk::MixSmem<DP, DU, Q, G::E>::BYTES;
+  k.smem_mf = fk::MixSmem<DP, DU, Q, G::E, true>::BYTES;
   k.f_both = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true>);
   k.f_tau = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false>);
   k.f_vb = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true>);
+  k.f_mf = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true>);
   k.launch = &mix_launch<DP, DU, Q, CFG>;
   return k;
 }
@@ -254,7 +263,7 @@ struct fk_mix {
   std::vector<double> Bp, Gp, Bu, w, rho, kinv;
   const MixKernel* kern = nullptr;
   cudaStream_t stream = nullptr;
-  int device = 0, num_sms = 0, blocks = 0;
+  int device = 0, num_sms = 0, blocks = 0, blocks_mf = 0;
   bool is_setup = false;
   int* gids = nullptr;
   double* pa = nullptr;
@@ -281,7 +290,10 @@ int mix_launch_mode(fk_mix* m, const double* u, const double* p, double* out_u, 
   a.su = su;
   a.sp = sp;
   a.nel = (int)m->nel;
-  m->kern->launch(*m->kern, m->Bp.data(), m->Gp.data(), m->Bu.data(), a, mode, m->blocks, s);
+  const double jinv[3] = {1.0 / m->desc.jac_diag[0], 1.0 / m->desc.jac_diag[1],
+                          1.0 / m->desc.jac_diag[2]};
+  m->kern->launch(*m->kern, m->Bp.data(), m->Gp.data(), m->Bu.data(), m->w.data(),
+                  m->desc.jac_det, jinv, a, mode, mode == MIX_BOTH_MF ? m->blocks_mf : m->blocks, s);
   FK_CUDA(cudaGetLastError());
   return FK_OK;
 }
@@ -291,7 +303,8 @@ int mix_apply_dev(fk_mix* m, const double* u, const double* p, double* out_u, do
                   cudaStream_t s) {
   FK_CUDA(cudaMemsetAsync(out_p, 0, sizeof(double) * m->ndof_p, s));
   const double cs = m->desc.coupling_scale;
-  return mix_launch_mode(m, u, p, out_u, out_p, MIX_BOTH, cs, -cs, s);
+  return mix_launch_mode(m, u, p, out_u, out_p, m->desc.matrix_free ? MIX_BOTH_MF : MIX_BOTH, cs,
+                         -cs, s);
 }
 
 }  // namespace
@@ -416,11 +429,15 @@ int fk_mix_setup(fk_mix* m) {
   cudaFree(d_kinv);
   for (const void* f : {k.f_both, k.f_tau, k.f_vb})
     FK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
-  int occ = 0;
+  FK_CUDA(cudaFuncSetAttribute(k.f_mf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem_mf));
+  int occ = 0, occ_mf = 0;
   FK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.f_both, k.T, k.smem));
-  if (occ < 1) return fk_fail(FK_EUNSUPPORTED, "mixed kernel does not fit on an SM (smem %zu)", k.smem);
+  FK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_mf, k.f_mf, k.T, k.smem_mf));
+  if (occ < 1 || occ_mf < 1)
+    return fk_fail(FK_EUNSUPPORTED, "mixed kernel does not fit on an SM (smem %zu)", k.smem);
   const int64_t nbatch = (m->nel + k.E - 1) / k.E;
   m->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ * m->num_sms));
+  m->blocks_mf = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ_mf * m->num_sms));
   for (auto& e : m->ev) FK_CUDA(cudaEventCreate(&e));
   m->is_setup = true;
   return FK_OK;
@@ -434,7 +451,7 @@ int fk_mix_get_info(const fk_mix* m, fk_mix_info* info) {
   info->pa_bytes = (int64_t)sizeof(double) * m->nel * m->kern->ps;
   info->elems_per_block = m->kern->E;
   info->threads_per_block = m->kern->T;
-  info->blocks = m->blocks;
+  info->blocks = m->desc.matrix_free ? m->blocks_mf : m->blocks;
   info->smem_bytes = (int64_t)m->kern->smem;
   return FK_OK;
 }
@@ -550,7 +567,8 @@ int fk_mix_time_apply(fk_mix* m, const double* u, const double* p, double* out_u
     FK_CUDA(cudaEventRecord(ev[3 * r], m->stream));
     FK_CUDA(cudaMemsetAsync(out_p, 0, sizeof(double) * m->ndof_p, m->stream));
     FK_CUDA(cudaEventRecord(ev[3 * r + 1], m->stream));
-    FK_TRY(mix_launch_mode(m, u, p, out_u, out_p, MIX_BOTH, cs, -cs, m->stream));
+    FK_TRY(mix_launch_mode(m, u, p, out_u, out_p, m->desc.matrix_free ? MIX_BOTH_MF : MIX_BOTH, cs,
+                           -cs, m->stream));
     FK_CUDA(cudaEventRecord(ev[3 * r + 2], m->stream));
   }
   FK_CUDA(cudaEventSynchronize(ev.back()));

@@ -41,6 +41,15 @@ struct __align__(16) MixTables {
   static constexpr int TBP = 0, TGP = FBp::SIZE, TBPT = 2 * FBp::SIZE, TGPT = TBPT + FBpT::SIZE;
   static constexpr int TBU = TGPT + FBpT::SIZE, TBUT = TBU + FBu::SIZE, SZ = TBUT + FBuT::SIZE;
   double t[SZ];
+  // matrix-free factors (FusedMF): 1D weights, |J|, 1/jac_diag
+  double mfw[Q + (Q & 1)];
+  double mfc[4];
+
+  void fill_mf(const double* w, double detj, const double* jinv) {
+    for (int a = 0; a < Q; ++a) mfw[a] = w[a];
+    mfc[0] = detj;
+    for (int s = 0; s < 3; ++s) mfc[1 + s] = jinv[s];
+  }
 
   // host: fold the reference tables (row-major q x d)
   void fill(const double* Bp, const double* Gp, const double* Bu) {
@@ -110,12 +119,12 @@ struct MixLayout {
   static constexpr int GS = ((DP3 + 3) / 4) * 4;
 };
 
-template <int DP, int DU, int Q, int E>
+template <int DP, int DU, int Q, int E, bool MF = false>
 struct MixSmem {
   using L = MixLayout<DP, DU, Q>;
   static constexpr size_t OFF_BAR = 0;  // 1 D barrier + 3 gid barriers
   static constexpr size_t OFF_DB = 32;
-  static constexpr size_t OFF_GS = OFF_DB + 8ull * E * L::PS;
+  static constexpr size_t OFF_GS = OFF_DB + (MF ? 0ull : 8ull * E * L::PS);
   static constexpr size_t OFF_R0 = OFF_GS + 4ull * 3 * E * L::GS;
   static constexpr size_t OFF_R1 = OFF_R0 + 8ull * E * L::R0S;
   static constexpr size_t OFF_XP = OFF_R1 + 8ull * E * L::R1S;
@@ -134,11 +143,14 @@ struct MixArgs {
   int nel;
 };
 
-template <int DP, int DU, int Q, int E, int T, bool TAU, bool VB>
+// MF (FusedMF strategy, operator.py:280-286): no dmat traffic — stage C
+// recomputes the diagonal w|J|J^-1 of the axis-aligned box from the 1D weights
+// in the PA setup's operation order.
+template <int DP, int DU, int Q, int E, int T, bool TAU, bool VB, bool MF = false>
 __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ MixTables<DP, DU, Q> tb,
                                                      const MixArgs arg) {
   using L = MixLayout<DP, DU, Q>;
-  using S = MixSmem<DP, DU, Q, E>;
+  using S = MixSmem<DP, DU, Q, E, MF>;
   using Tb = MixTables<DP, DU, Q>;
   constexpr int DP3 = L::DP3, DU3 = L::DU3, Q3 = L::Q3, GS = L::GS, PS = L::PS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -171,6 +183,7 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
     bulk_g2s(gs + slot * E * GS, arg.gids + (size_t)e0 * GS, bytes, bar_g + slot);
   };
   auto issue_d = [&](int b) {
+    if constexpr (MF) return;
     const int e0 = b * E, ne = min(E, nel - e0);
     const uint32_t bytes = 8u * ne * PS;
     mbar_expect_tx(bar_d, bytes);
@@ -309,13 +322,21 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
     });
     __syncthreads();
     // ---- stage C: z + D + z^T (D read once for both blocks)
-    mbar_wait(bar_d, ph_d);
-    ph_d ^= 1u;
+    if constexpr (!MF) {
+      mbar_wait(bar_d, ph_d);
+      ph_d ^= 1u;
+    }
     lines(ne, NCP, NCU, [&](int e, int l) {
       const bool pph = TAU && l < NCP;
       const int m = pph ? l : l - NCP;
       const int a = m % Q, b2 = m / Q;
-      const double* pe = db + e * PS + a + Q * b2;
+      const double* pe = MF ? nullptr : db + e * PS + a + Q * b2;
+      const double wab = MF ? tb.mfw[b2] * tb.mfw[a] : 0.0;
+      // dmat[s][r] at point c (9 components; MF: the box's diagonal)
+      auto dm = [&](int c, int s, int r) -> double {
+        if constexpr (MF) return s == r ? ((tb.mfw[c] * wab) * tb.mfc[0]) * tb.mfc[1 + s] : 0.0;
+        else return pe[c * Q * Q + (s * 3 + r) * Q3];
+      };
       if (TAU && pph) {
         double tin[3][DP], g0[Q], g1[Q], g2[Q];
 #pragma unroll
@@ -327,12 +348,11 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
         contract_eo<DP, Q, -1>(tab + Tb::TGP, tin[2], g2);
 #pragma unroll
         for (int c = 0; c < Q; ++c) {
-          const double* pc = pe + c * Q * Q;
           const double x0 = g0[c], x1 = g1[c], x2 = g2[c];
           // t_r = sum_s D[s][r] g_s  (einsum qsr,sq->rq, operator.py:294)
-          g0[c] = fma(pc[6 * Q3], x2, fma(pc[3 * Q3], x1, pc[0 * Q3] * x0));
-          g1[c] = fma(pc[7 * Q3], x2, fma(pc[4 * Q3], x1, pc[1 * Q3] * x0));
-          g2[c] = fma(pc[8 * Q3], x2, fma(pc[5 * Q3], x1, pc[2 * Q3] * x0));
+          g0[c] = fma(dm(c, 2, 0), x2, fma(dm(c, 1, 0), x1, dm(c, 0, 0) * x0));
+          g1[c] = fma(dm(c, 2, 1), x2, fma(dm(c, 1, 1), x1, dm(c, 0, 1) * x0));
+          g2[c] = fma(dm(c, 2, 2), x2, fma(dm(c, 1, 2), x1, dm(c, 0, 2) * x0));
         }
         double w[DU];
         contract_eo<Q, DU, +1>(tab + Tb::TBUT, g0, w);
@@ -355,12 +375,11 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
         contract_eo<DU, Q, +1>(tab + Tb::TBU, tin[2], u2);
 #pragma unroll
         for (int c = 0; c < Q; ++c) {
-          const double* pc = pe + c * Q * Q;
           const double x0 = u0[c], x1 = u1[c], x2 = u2[c];
           // t_s = sum_r D[s][r] u_r  (einsum qsr,rq->sq, operator.py:316)
-          u0[c] = fma(pc[2 * Q3], x2, fma(pc[1 * Q3], x1, pc[0 * Q3] * x0));
-          u1[c] = fma(pc[5 * Q3], x2, fma(pc[4 * Q3], x1, pc[3 * Q3] * x0));
-          u2[c] = fma(pc[8 * Q3], x2, fma(pc[7 * Q3], x1, pc[6 * Q3] * x0));
+          u0[c] = fma(dm(c, 0, 2), x2, fma(dm(c, 0, 1), x1, dm(c, 0, 0) * x0));
+          u1[c] = fma(dm(c, 1, 2), x2, fma(dm(c, 1, 1), x1, dm(c, 1, 0) * x0));
+          u2[c] = fma(dm(c, 2, 2), x2, fma(dm(c, 2, 1), x1, dm(c, 2, 0) * x0));
         }
         double w[DP];
         contract_eo<Q, DP, +1>(tab + Tb::TBPT, u0, w);

@@ -24,7 +24,9 @@ import numpy as np
 from . import _lib
 from .fem import Basis1D, Counters, h1_gather_ids
 
-STRATEGIES = ("PA", "FusedPA")
+# PA / FusedPA: stored dmat (one fused pass reads it once for both blocks);
+# MF / FusedMF: dmat recomputed in the kernel (operator.py:16-19, 280-286)
+STRATEGIES = ("PA", "FusedPA", "MF", "FusedMF")
 
 
 def _torch():
@@ -58,8 +60,8 @@ class MixedOperator:
 
     Supported: order_u = order_p - 1, num_quad_1d = order_p + 1, order_p = 2..8
     (the reference default 4/3/5), scalar or per-element rho / bulk modulus,
-    coupling_scale.  Not supported (raise): absorbing faces, surface gravity,
-    the "MF"/"FusedMF" strategies (operator.py:400-440, :280-286).
+    coupling_scale.  Not supported (raise): absorbing faces, surface gravity
+    (operator.py:400-440).  strategy MF / FusedMF recomputes dmat in the kernel.
     """
 
     def __init__(self, mesh, order_p: int = 4, order_u: int = 3, num_quad_1d: int = 5,
@@ -109,6 +111,7 @@ class MixedOperator:
         desc.bulk = bulk_a.ctypes.data_as(pd)
         desc.rho_scalar = desc.bulk_scalar = 1.0
         desc.coupling_scale = self.coupling_scale
+        desc.matrix_free = 1 if strategy in ("MF", "FusedMF") else 0
         desc.device = self.device.index
         desc.stream = ctypes.c_void_p(self._stream.cuda_stream)
         h = ctypes.c_void_p()
@@ -250,9 +253,10 @@ class MixedOperator:
     @property
     def bytes_per_apply(self) -> int:
         """u read + out_u write (48 du^3 per element), p read + out_p write
-        (16 per H1 dof), dmat (72 q^3), int32 map (4 dp^3) per element."""
+        (16 per H1 dof), dmat (72 q^3; not for MF), int32 map (4 dp^3) per element."""
         du3, dp3, q3 = (self.order_u + 1) ** 3, (self.order_p + 1) ** 3, self.num_quad_1d ** 3
-        return self.num_elements * (48 * du3 + 72 * q3 + 4 * dp3) + 16 * self.num_p
+        dm = 0 if self.strategy in ("MF", "FusedMF") else 72 * q3
+        return self.num_elements * (48 * du3 + dm + 4 * dp3) + 16 * self.num_p
 
     def gather_ids(self) -> np.ndarray:
         return h1_gather_ids(self.mesh.nx, self.mesh.ny, self.mesh.nz, self.order_p + 1)

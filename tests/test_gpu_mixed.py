@@ -36,11 +36,12 @@ def make(golden, name, **kw):
                          bulk_modulus=float(m[10]), coupling_scale=float(m[11]), **kw)
 
 
+@pytest.mark.parametrize("strategy", ["FusedPA", "PA", "FusedMF", "MF"])
 @pytest.mark.parametrize("name", CASES)
-def test_apply_matches_reference(golden, name):
+def test_apply_matches_reference(golden, name, strategy):
     from paper_2603_09038_b200 import MixedState
 
-    op = make(golden, name)
+    op = make(golden, name, strategy=strategy)
     r = op.apply(MixedState(golden[f"{name}_u"], golden[f"{name}_p"]))
     assert normwise(r.u, golden[f"{name}_FusedPA_out_u"]) <= TOL
     assert normwise(r.p, golden[f"{name}_FusedPA_out_p"]) <= TOL
@@ -94,6 +95,10 @@ def test_every_order_vs_oracle(order_p):
     assert normwise(r.u, ru) <= TOL
     assert normwise(r.p, rp) <= TOL
     assert normwise(op.apply_fused_normal(u), P.fused_normal(u)) <= TOL
+    mf = MixedOperator(build_mesh(*n, extents=ext), order_p, order_p - 1, order_p + 1, rho=rho,
+                       bulk_modulus=2.0, coupling_scale=0.75, strategy="FusedMF")
+    r = mf.apply(MixedState(u, p))
+    assert normwise(r.u, ru) <= TOL and normwise(r.p, rp) <= TOL
     lu, lp = op.lumped()
     assert normwise(lu, P.lump_u) <= 1e-14 and normwise(lp, P.lump_p) <= 1e-14
 
