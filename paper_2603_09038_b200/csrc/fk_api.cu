@@ -61,7 +61,7 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // (tools/auto_table.py)
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg3[9] = {0, 14, 1, 11, 1, 1, 14, 18, 10};
+const int kAutoCfg3[9] = {0, 14, 1, 11, 5, 1, 14, 18, 10};  // p=4: eo5, 3 repeated sweeps (r01_sweep_v15_p4_reps)
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
 const int kAutoCfg1[9] = {0, 9, 6, 9, 2, 18, 10, 14, 14};
 
