@@ -212,30 +212,31 @@ __global__ void mix_minv_kernel(double* __restrict__ ku, const double* __restric
                                 const double* __restrict__ lump_p, int64_t np, double sign) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nu + np;
        t += (int64_t)gridDim.x * blockDim.x) {
-    if (t < nu) ku[t] = (sign * ru[t]) / lump_u[t % nel_du3];
+    if (t < nu) ku[t] = (sign * ru[t]) / lump_u[t - (t >= nel_du3 ? (t >= 2 * nel_du3 ? 2 : 1) : 0) * nel_du3];
     else kp[t - nu] = (sign * rp[t - nu]) / lump_p[t - nu];
   }
 }
 
-// y = x + c k, two separately rounded operations like NumPy (state_lincomb)
-__global__ void mix_axpy_kernel(double* __restrict__ y, const double* __restrict__ x,
-                                const double* __restrict__ k, double c, int64_t n) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    y[t] = __dadd_rn(x[t], __dmul_rn(c, k[t]));
-}
-
-// y = (((y + c1 k1) + c2 k2) + c3 k3) + c4 k4 (the final lincomb, left to right)
-__global__ void mix_rk4_final_kernel(double* __restrict__ y, const double* __restrict__ k1,
-                                     const double* __restrict__ k2, const double* __restrict__ k3,
-                                     const double* __restrict__ k4, double c1, double c2, double c3,
-                                     double c4, int64_t n) {
+// One fused RK4 stage update (rk4_step, operator.py:506-531) on [u | p]:
+//   k    = (-r) / lump                      (rhs negation + apply_mass_inverse)
+//   acc' = (first ? y : acc) + c_acc * k    (the final lincomb, accumulated in
+//                                            the reference's left-to-right order)
+//   ynext = y + c_next * k                  (next stage state; skipped if c_next == 0)
+// Every multiply and add separately rounded, like NumPy.  k is never stored.
+__global__ void mix_rk4_stage_kernel(const double* __restrict__ r, const double* __restrict__ lump_u,
+                                     int64_t nu, int64_t nel_du3, const double* __restrict__ lump_p,
+                                     const double* y, const double* acc_in, double* acc_out,
+                                     double* __restrict__ ynext, double c_acc, double c_next,
+                                     int first, int64_t n) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
-    double v = __dadd_rn(y[t], __dmul_rn(c1, k1[t]));
-    v = __dadd_rn(v, __dmul_rn(c2, k2[t]));
-    v = __dadd_rn(v, __dmul_rn(c3, k3[t]));
-    y[t] = __dadd_rn(v, __dmul_rn(c4, k4[t]));
+    // u is (3, nel, du^3): its lumped entry is lump_u[t - r nel du^3] (no 64-bit modulo)
+    const double lump = t < nu ? lump_u[t - (t >= nel_du3 ? (t >= 2 * nel_du3 ? 2 : 1) : 0) * nel_du3]
+                               : lump_p[t - nu];
+    const double k = (-r[t]) / lump;
+    const double yt = y[t];
+    acc_out[t] = __dadd_rn(first ? yt : acc_in[t], __dmul_rn(c_acc, k));
+    if (c_next != 0.0) ynext[t] = __dadd_rn(yt, __dmul_rn(c_next, k));
   }
 }
 
@@ -494,39 +495,32 @@ int fk_mix_rk4(fk_mix* m, double* u, double* p, double dt, int steps) {
   if (steps < 0) return fk_fail(FK_EINVAL, "steps must be >= 0");
   FkDeviceGuard g(m->device);
   const int64_t nu = nu_of(m), n = nu + m->ndof_p, du3 = m->du * m->du * m->du;
-  // state layout [u | p] in one buffer per stage vector
-  if (m->rk == nullptr) FK_CUDA(cudaMalloc(&m->rk, sizeof(double) * 7 * n));
-  double* k[4] = {m->rk, m->rk + n, m->rk + 2 * n, m->rk + 3 * n};
-  double* tmp = m->rk + 4 * n;
-  double* res = m->rk + 5 * n;
+  // work vectors [u | p]: y (state), acc (final lincomb), ytmp (stage state), r (residual)
+  if (m->rk == nullptr) FK_CUDA(cudaMalloc(&m->rk, sizeof(double) * 4 * n));
+  double* y = m->rk;
+  double* acc = m->rk + n;
+  double* ytmp = m->rk + 2 * n;
+  double* res = m->rk + 3 * n;
   cudaStream_t s = m->stream;
   const int gb = grid_for(n, 256, m->num_sms);
-  auto rhs = [&](const double* yu, const double* yp, double* kk) -> int {
-    FK_TRY(mix_apply_dev(m, yu, yp, res, res + nu, s));
-    mix_minv_kernel<<<gb, 256, 0, s>>>(kk, res, m->lump_u, nu, m->nel * du3, kk + nu, res + nu,
-                                        m->lump_p, m->ndof_p, -1.0);
+  // one stage: r = A x, then the fused k / acc / next-state update
+  auto stage = [&](const double* x, double c_acc, double c_next, int first, double* acc_out) -> int {
+    FK_TRY(mix_apply_dev(m, x, x + nu, res, res + nu, s));
+    mix_rk4_stage_kernel<<<gb, 256, 0, s>>>(res, m->lump_u, nu, m->nel * du3, m->lump_p, y, acc,
+                                            acc_out, ytmp, c_acc, c_next, first, n);
     FK_CUDA(cudaGetLastError());
     return FK_OK;
   };
-  // the state [u | p] lives in one work vector (u and p are separate user buffers)
-  double* y = tmp;
-  double* ybuf = m->rk + 6 * n;
-  FK_CUDA(cudaMemcpyAsync(ybuf, u, sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
-  FK_CUDA(cudaMemcpyAsync(ybuf + nu, p, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(y, u, sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(y + nu, p, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice, s));
   for (int st = 0; st < steps; ++st) {
-    FK_TRY(rhs(ybuf, ybuf + nu, k[0]));
-    mix_axpy_kernel<<<gb, 256, 0, s>>>(y, ybuf, k[0], dt / 2, n);
-    FK_TRY(rhs(y, y + nu, k[1]));
-    mix_axpy_kernel<<<gb, 256, 0, s>>>(y, ybuf, k[1], dt / 2, n);
-    FK_TRY(rhs(y, y + nu, k[2]));
-    mix_axpy_kernel<<<gb, 256, 0, s>>>(y, ybuf, k[2], dt, n);
-    FK_TRY(rhs(y, y + nu, k[3]));
-    mix_rk4_final_kernel<<<gb, 256, 0, s>>>(ybuf, k[0], k[1], k[2], k[3], dt / 6, dt / 3, dt / 3,
-                                             dt / 6, n);
-    FK_CUDA(cudaGetLastError());
+    FK_TRY(stage(y, dt / 6, dt / 2, 1, acc));     // k1
+    FK_TRY(stage(ytmp, dt / 3, dt / 2, 0, acc));  // k2
+    FK_TRY(stage(ytmp, dt / 3, dt, 0, acc));      // k3
+    FK_TRY(stage(ytmp, dt / 6, 0.0, 0, y));       // k4: y = acc + dt/6 k4
   }
-  FK_CUDA(cudaMemcpyAsync(u, ybuf, sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
-  FK_CUDA(cudaMemcpyAsync(p, ybuf + nu, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(u, y, sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
+  FK_CUDA(cudaMemcpyAsync(p, y + nu, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice, s));
   return FK_OK;
 }
 
