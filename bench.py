@@ -39,7 +39,7 @@ UNIT = "GDOF/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kind", default="diffusion", choices=["diffusion", "mass"])
@@ -107,6 +107,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi needs a moment to start: wait (bounded) for its first
+            # sample so the (short) timed region that follows is covered
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -122,6 +128,9 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+
+    def count(self) -> int:
+        return len(self.lines)
 
     def summary(self):
         sm, smax, reasons = [], None, set()
@@ -296,9 +305,16 @@ def run_ours(a):
         barrier()
         ms = ev0.elapsed_time(ev1) / a.steps
         # kernel-only timing for the roofline (events around the fused kernel,
-        # on the operator's stream)
-        reps = min(a.steps, 50)
+        # on the operator's stream; median over the reps)
+        reps = max(20, min(a.steps, 100))
         _, ms_kernel = op.time_apply(x, y, reps)
+        # keep the same load until nvidia-smi has >= 3 samples (clock check only;
+        # nothing here is timed)
+        t_hold = time.time()
+        while sampler.count() < 3 and time.time() - t_hold < 2.0:
+            for _ in range(20):
+                op.apply(x, out=y)
+            torch.cuda.synchronize()
     ms = max_over_ranks(ms)
     ms_kernel = max_over_ranks(ms_kernel)
     ndof_global = op.num_global_dofs
@@ -325,6 +341,7 @@ def run_ours(a):
     achieved = alg_bytes / (ms_kernel * 1e-3) / 1e9
     traffic = ncu_traffic(a.kind, p, n)
     clocks = sampler.summary()
+    clocks["window"] = "nvidia-smi -lms 50 from warm-up start to the end of the kernel timing"
     sweep = None
     if a.sweep and rank == 0 and world == 1:
         sweep = run_sweep(a, peak)

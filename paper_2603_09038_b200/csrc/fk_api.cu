@@ -788,21 +788,21 @@ int fk_op_time_apply(fk_op* op, const double* x, double* y, int reps, const void
           y, x, op->ess, op->n_ess);
     FK_CUDA(cudaEventRecord(e[3], op->stream));
   }
-  double tot_a = 0.0, tot_k = 0.0;
+  // medians over the reps (robust to a stray slow rep, e.g. a clock change)
+  std::vector<float> ta(reps), tk(reps);
   if (rc == FK_OK) {
     FK_CUDA(cudaEventSynchronize(ev[4 * (size_t)reps - 1]));
     for (int r = 0; r < reps; ++r) {
-      float a = 0.f, k = 0.f;
-      FK_CUDA(cudaEventElapsedTime(&a, ev[4 * r], ev[4 * r + 3]));
-      FK_CUDA(cudaEventElapsedTime(&k, ev[4 * r + 1], ev[4 * r + 2]));
-      tot_a += a;
-      tot_k += k;
+      FK_CUDA(cudaEventElapsedTime(&ta[r], ev[4 * r], ev[4 * r + 3]));
+      FK_CUDA(cudaEventElapsedTime(&tk[r], ev[4 * r + 1], ev[4 * r + 2]));
     }
   }
   for (auto& e : ev) cudaEventDestroy(e);
   if (rc != FK_OK) return rc;
-  if (ms_apply) *ms_apply = tot_a / reps;
-  if (ms_kernel) *ms_kernel = tot_k / reps;
+  std::sort(ta.begin(), ta.end());
+  std::sort(tk.begin(), tk.end());
+  if (ms_apply) *ms_apply = ta[reps / 2];
+  if (ms_kernel) *ms_kernel = tk[reps / 2];
   return FK_OK;
 }
 
