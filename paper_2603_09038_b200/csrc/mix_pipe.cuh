@@ -70,9 +70,38 @@ struct __align__(16) MixTables {
   }
 };
 
+// Strides of the intermediate buffers, word = c*CS + i1*S1 + i2*S2 + i3*S3
+// with (i1, i2, i3) = (a, j, k) for T1/R and (a, b, k) for T2/W.  The
+// primary template is the odd-pitch line layout; mix_layouts.cuh specialises
+// it with strides searched by tools/mix_strides.py (bank-conflict-free).
+template <int CS, int S1, int S2, int S3>
+struct SStr {
+  static constexpr int cs = CS, s1 = S1, s2 = S2, s3 = S3;
+};
+
+template <int DP, int DU, int Q>
+struct MixStrides {
+  static constexpr int LSP = DP | 1, LSU = DU | 1, LQ = Q | 1;
+  using T1P = SStr<Q * DP * LSP, DP * LSP, 1, LSP>;
+  using T1U = SStr<Q * DU * LSU, DU * LSU, 1, LSU>;
+  using T2P = SStr<Q * Q * LSP, LSP, Q * LSP, 1>;
+  using T2U = SStr<Q * Q * LSU, LSU, Q * LSU, 1>;
+  using WP = SStr<DP * Q * LQ, LQ, 1, Q * LQ>;
+  using WU = SStr<DU * Q * LQ, LQ, 1, Q * LQ>;
+  using RP = SStr<DP * DP * LQ, 1, LQ, DP * LQ>;
+  using RU = SStr<DU * DU * LQ, 1, LQ, DU * LQ>;
+};
+
+}  // namespace fk
+
+#include "mix_layouts.cuh"
+
+namespace fk {
+
 // Shared-memory and global layouts of one (DP, DU, Q) instance.
 template <int DP, int DU, int Q>
 struct MixLayout {
+  using St = MixStrides<DP, DU, Q>;
   static constexpr int LSP = DP | 1, LSU = DU | 1, LQ = Q | 1;
   static constexpr int DP3 = DP * DP * DP, DU3 = DU * DU * DU, Q3 = Q * Q * Q;
   // X buffers
@@ -82,37 +111,39 @@ struct MixLayout {
   __device__ __forceinline__ static int xu(int e, int r, int i, int j, int k) {
     return e * XUS + r * XUC + i + LSU * (j + DU * k);
   }
+  template <class S>
+  __device__ __forceinline__ static int w(int c, int i1, int i2, int i3) {
+    return c * S::cs + i1 * S::s1 + i2 * S::s2 + i3 * S::s3;
+  }
   // region 1: T1p (2), T1u (3), later Wp (3), Wu (3)
-  static constexpr int T1PC = Q * DP * LSP, T1UC = Q * DU * LSU, OFF_T1U = 2 * T1PC;
-  static constexpr int WPC = DP * Q * LQ, WUC = DU * Q * LQ, OFF_WU = 3 * WPC;
-  static constexpr int R1S = odd_up(cmax(2 * T1PC + 3 * T1UC, 3 * WPC + 3 * WUC));
+  static constexpr int OFF_T1U = 2 * St::T1P::cs, OFF_WU = 3 * St::WP::cs;
+  static constexpr int R1S = odd_up(cmax(2 * St::T1P::cs + 3 * St::T1U::cs, 3 * St::WP::cs + 3 * St::WU::cs));
   __device__ __forceinline__ static int t1p(int e, int s, int a, int j, int k) {
-    return e * R1S + s * T1PC + a * DP * LSP + j + LSP * k;
+    return e * R1S + w<typename St::T1P>(s, a, j, k);
   }
   __device__ __forceinline__ static int t1u(int e, int r, int a, int j, int k) {
-    return e * R1S + OFF_T1U + r * T1UC + a * DU * LSU + j + LSU * k;
+    return e * R1S + OFF_T1U + w<typename St::T1U>(r, a, j, k);
   }
   __device__ __forceinline__ static int wp(int e, int s, int a, int b, int k) {
-    return e * R1S + s * WPC + a * LQ + b + Q * LQ * k;
+    return e * R1S + w<typename St::WP>(s, a, b, k);
   }
   __device__ __forceinline__ static int wu(int e, int r, int a, int b, int k) {
-    return e * R1S + OFF_WU + r * WUC + a * LQ + b + Q * LQ * k;
+    return e * R1S + OFF_WU + w<typename St::WU>(r, a, b, k);
   }
   // region 0: T2p (3), T2u (3), later Rp (2), Ru (3)
-  static constexpr int T2PC = Q * Q * LSP, T2UC = Q * Q * LSU, OFF_T2U = 3 * T2PC;
-  static constexpr int RPC = DP * DP * LQ, RUC = DU * DU * LQ, OFF_RU = 2 * RPC;
-  static constexpr int R0S = odd_up(cmax(3 * T2PC + 3 * T2UC, 2 * RPC + 3 * RUC));
+  static constexpr int OFF_T2U = 3 * St::T2P::cs, OFF_RU = 2 * St::RP::cs;
+  static constexpr int R0S = odd_up(cmax(3 * St::T2P::cs + 3 * St::T2U::cs, 2 * St::RP::cs + 3 * St::RU::cs));
   __device__ __forceinline__ static int t2p(int e, int s, int a, int b, int k) {
-    return e * R0S + s * T2PC + a * LSP + Q * LSP * b + k;
+    return e * R0S + w<typename St::T2P>(s, a, b, k);
   }
   __device__ __forceinline__ static int t2u(int e, int r, int a, int b, int k) {
-    return e * R0S + OFF_T2U + r * T2UC + a * LSU + Q * LSU * b + k;
+    return e * R0S + OFF_T2U + w<typename St::T2U>(r, a, b, k);
   }
   __device__ __forceinline__ static int rp(int e, int s, int a, int j, int k) {
-    return e * R0S + s * RPC + a + LQ * j + DP * LQ * k;
+    return e * R0S + w<typename St::RP>(s, a, j, k);
   }
   __device__ __forceinline__ static int ru(int e, int r, int a, int j, int k) {
-    return e * R0S + OFF_RU + r * RUC + a + LQ * j + DU * LQ * k;
+    return e * R0S + OFF_RU + w<typename St::RU>(r, a, j, k);
   }
   // global: PA data 9 components per point, int32 gather ids
   static constexpr int PS = pa_pad(((9 * Q3 + 1) / 2) * 2, Q);
