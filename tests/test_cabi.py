@@ -113,3 +113,41 @@ def test_bench_module_imports():
     finally:
         sys.argv = argv
     assert a.steps == 3 and a.impl == "ours"
+
+
+def _mix_desc(**kw):
+    d = _lib.FkMixDesc()
+    d.order_p, d.order_u, d.num_quad_1d = 4, 3, 5
+    d.nx = d.ny = d.nz = 2
+    for s in range(3):
+        d.jac_diag[s] = 0.25
+    d.jac_det = 0.25 ** 3
+    T = np.zeros((5, 5))
+    dp = ctypes.POINTER(ctypes.c_double)
+    d._keep = T
+    d.Bp = d.Gp = d.Bu = d.w = T.ctypes.data_as(dp)
+    d.rho_scalar = d.bulk_scalar = 1.0
+    d.coupling_scale = 1.0
+    for k, v in kw.items():
+        setattr(d, k, v)
+    return d
+
+
+@pytest.mark.parametrize("kw,code,needle", [
+    (dict(order_p=1, order_u=0, num_quad_1d=2), _lib.FK_EUNSUPPORTED, "order_p"),
+    (dict(order_u=2), _lib.FK_EUNSUPPORTED, "order_u"),
+    (dict(num_quad_1d=6), _lib.FK_EUNSUPPORTED, "q"),
+    (dict(nz=0), _lib.FK_EINVAL, "do not match"),
+    (dict(jac_det=0.0), _lib.FK_EINVAL, "Jacobian"),
+    (dict(rho_scalar=-1.0), _lib.FK_EINVAL, "positive"),
+])
+def test_mix_create_validates(kw, code, needle):
+    """fk_mix_create (acoustic-gravity operator) validates the descriptor on the
+    host, with the reference's wording where it has one (operator.py:129-130,
+    160-161)."""
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    d = _mix_desc(**kw)
+    rc = lib.fk_mix_create(ctypes.byref(h), ctypes.byref(d))
+    assert rc == code
+    assert needle in lib.fk_last_error().decode()
