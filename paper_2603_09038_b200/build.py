@@ -56,6 +56,7 @@ def sources():
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(HERE, "..", "include", "fk.h"))
     units = [(f"pa_p{p}", "pa_inst.cu", [f"-DFK_P={p}"]) for p in ORDERS]
+    units += [(f"mix_p{p}", "mix_inst.cu", [f"-DFK_MIX_P={p}"]) for p in range(2, 9)]
     units += [("fk_api", "fk_api.cu", []), ("fk_comm", "fk_comm.cu", []), ("fk_mixed", "fk_mixed.cu", [])]
     return units, deps
 

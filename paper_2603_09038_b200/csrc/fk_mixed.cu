@@ -12,125 +12,37 @@
 #include <vector>
 
 #include "fk_error.h"
-#include "mix_pipe.cuh"
+#include "mix_kernels.h"
 
 namespace {
 
 using fk::MixArgs;
+using fk::MixKernel;
+using fk::MIX_BOTH;
+using fk::MIX_TAU;
+using fk::MIX_VB;
+using fk::MIX_BOTH_MF;
+using fk::kMixCfgs;
 
 // Compiled (order_p, order_u, q): the paper's H1(p) x L2(p-1) pairs with
 // q = p+1 (the reference default is p=4, u=3, q=5, operator.py:227-229).
 constexpr int kMixMaxP = 8;
 
-struct MixKernel {
-  int dp = 0, du = 0, q = 0, cfg = 0, E = 0, T = 0, ps = 0, gs = 0;
-  size_t smem = 0, smem_mf = 0;
-  const void* f_both = nullptr;
-  const void* f_tau = nullptr;
-  const void* f_vb = nullptr;
-  const void* f_mf = nullptr;  // FusedMF apply (both blocks, no dmat traffic)
-  void (*launch)(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
-                 const double* w, double detj, const double* jinv, const MixArgs& a, int mode,
-                 int blocks, cudaStream_t s) = nullptr;
-};
-
-enum { MIX_BOTH = 0, MIX_TAU = 1, MIX_VB = 2, MIX_BOTH_MF = 3 };
-
-constexpr int round32(int n) { return (n + 31) / 32 * 32; }
-constexpr int cmax5(int a, int b, int c, int d, int e) {
-  return fk::cmax(fk::cmax(a, b), fk::cmax(c, fk::cmax(d, e)));
-}
-
-// Launch geometries: E ~ EB / NMAX elements per CTA (NMAX = lines of the
-// widest stage), one thread per line of the widest stage (measured: fewer
-// threads, e.g. one per stage-C line, is slower at every order)
-template <int DP, int DU, int Q, int CFG>
-struct MixGeom {
-  static constexpr int NA = DP * DP + 3 * DU * DU, NB = Q * DP + 3 * Q * DU, NC = 2 * Q * Q;
-  static constexpr int NMAX = NB > NA ? (NB > NC ? NB : NC) : (NA > NC ? NA : NC);
-  static constexpr int EB = CFG == 1 ? 384 : CFG == 2 ? 96 : CFG == 3 ? 288 : 192;
-  static constexpr int E = EB / NMAX > 0 ? EB / NMAX : 1;
-  // one thread per line of the widest stage, the two blocks' lines of a stage
-  // laid out warp-aligned (mix_pipe.cuh lines())
-  static constexpr int PA_ = round32(E * DP * DP) + E * 3 * DU * DU;
-  static constexpr int PB_ = round32(E * Q * DP) + E * 3 * Q * DU;
-  static constexpr int PC_ = round32(E * Q * Q) + E * Q * Q;
-  static constexpr int PD_ = round32(E * 3 * Q * DU) + E * Q * DP;
-  static constexpr int PE_ = round32(E * 3 * DU * DU) + E * DP * DP;
-  static constexpr int TL = cmax5(PA_, PB_, PC_, PD_, PE_);
-  static constexpr int T = round32(TL) > 384 ? 384 : round32(TL);
-};
-constexpr int kMixCfgs = 4;
-
-template <int DP, int DU, int Q, int CFG>
-void mix_launch(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
-                const double* w, double detj, const double* jinv, const MixArgs& a, int mode,
-                int blocks, cudaStream_t s) {
-  using G = MixGeom<DP, DU, Q, CFG>;
-  fk::MixTables<DP, DU, Q> tb;
-  tb.fill(Bp, Gp, Bu);
-  tb.fill_mf(w, detj, jinv);
-  const size_t smem = fk::MixSmem<DP, DU, Q, G::E>::BYTES;
-  if (mode == MIX_BOTH)
-    fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true><<<blocks, G::T, smem, s>>>(tb, a);
-  else if (mode == MIX_TAU)
-    fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false><<<blocks, G::T, smem, s>>>(tb, a);
-  else if (mode == MIX_VB)
-    fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true><<<blocks, G::T, smem, s>>>(tb, a);
-  else
-    fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true>
-        <<<blocks, G::T, fk::MixSmem<DP, DU, Q, G::E, true>::BYTES, s>>>(tb, a);
-}
-
-template <int P, int CFG>
-MixKernel mix_entry() {
-  constexpr int DP = P + 1, DU = P, Q = P + 1;
-  using G = MixGeom<DP, DU, Q, CFG>;
-  using L = fk::MixLayout<DP, DU, Q>;
-  MixKernel k;
-  k.dp = DP;
-  k.du = DU;
-  k.q = Q;
-  k.cfg = CFG;
-  k.E = G::E;
-  k.T = G::T;
-  k.ps = L::PS;
-  k.gs = L::GS;
-  k.smem = fk::MixSmem<DP, DU, Q, G::E>::BYTES;
-  k.smem_mf = fk::MixSmem<DP, DU, Q, G::E, true>::BYTES;
-  k.f_both = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true>);
-  k.f_tau = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false>);
-  k.f_vb = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true>);
-  k.f_mf = reinterpret_cast<const void*>(&fk::mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true>);
-  k.launch = &mix_launch<DP, DU, Q, CFG>;
-  return k;
-}
-
-template <int P>
-void mix_add(std::vector<MixKernel>& v) {
-  v.push_back(mix_entry<P, 0>());
-  v.push_back(mix_entry<P, 1>());
-  v.push_back(mix_entry<P, 2>());
-  v.push_back(mix_entry<P, 3>());
-}
-
 const std::vector<MixKernel>& mix_registry() {
   static const std::vector<MixKernel> reg = [] {
     std::vector<MixKernel> v;
-    mix_add<2>(v);
-    mix_add<3>(v);
-    mix_add<4>(v);
-    mix_add<5>(v);
-    mix_add<6>(v);
-    mix_add<7>(v);
-    mix_add<8>(v);
+    fk_mix_register_p2(v);
+    fk_mix_register_p3(v);
+    fk_mix_register_p4(v);
+    fk_mix_register_p5(v);
+    fk_mix_register_p6(v);
+    fk_mix_register_p7(v);
+    fk_mix_register_p8(v);
     return v;
   }();
   return reg;
 }
 
-// default geometry per order_p (index = order_p): fastest in the bench --mixed
-// sweep (tools/gpu_mixsweep.sh, profiles/r01_mixed_sweep_v3_warp_aligned.jsonl)
 const int kMixAutoCfg[9] = {0, 0, 0, 3, 2, 2, 0, 0, 0};
 
 int grid_for(int64_t n, int threads, int num_sms) {

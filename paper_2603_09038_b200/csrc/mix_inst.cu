@@ -1,0 +1,88 @@
+// mix_inst.cu — instantiation of the acoustic-gravity kernels for ONE order
+// (compiled once per order with -DFK_MIX_P=<order_p>; the build runs them in
+// parallel).  Exports fk_mix_register_p<order_p>().
+#include "mix_kernels.h"
+
+#ifndef FK_MIX_P
+#error "compile with -DFK_MIX_P=<order_p>"
+#endif
+
+namespace fk {
+namespace {
+
+template <int DP, int DU, int Q, int CFG>
+struct MixGeom {
+  static constexpr int NA = DP * DP + 3 * DU * DU, NB = Q * DP + 3 * Q * DU, NC = 2 * Q * Q;
+  static constexpr int NMAX = NB > NA ? (NB > NC ? NB : NC) : (NA > NC ? NA : NC);
+  static constexpr int EB = CFG == 1 ? 384 : CFG == 2 ? 96 : CFG == 3 ? 288 : 192;
+  static constexpr int E = EB / NMAX > 0 ? EB / NMAX : 1;
+  // one thread per line of the widest stage, the two blocks' lines of a stage
+  // laid out warp-aligned (mix_pipe.cuh lines())
+  static constexpr int PA_ = mix_round32(E * DP * DP) + E * 3 * DU * DU;
+  static constexpr int PB_ = mix_round32(E * Q * DP) + E * 3 * Q * DU;
+  static constexpr int PC_ = mix_round32(E * Q * Q) + E * Q * Q;
+  static constexpr int PD_ = mix_round32(E * 3 * Q * DU) + E * Q * DP;
+  static constexpr int PE_ = mix_round32(E * 3 * DU * DU) + E * DP * DP;
+  static constexpr int TL = cmax5(PA_, PB_, PC_, PD_, PE_);
+  static constexpr int T = mix_round32(TL) > 384 ? 384 : mix_round32(TL);
+};
+
+template <int DP, int DU, int Q, int CFG>
+void mix_launch(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
+                const double* w, double detj, const double* jinv, const MixArgs& a, int mode,
+                int blocks, cudaStream_t s) {
+  using G = MixGeom<DP, DU, Q, CFG>;
+  MixTables<DP, DU, Q> tb;
+  tb.fill(Bp, Gp, Bu);
+  tb.fill_mf(w, detj, jinv);
+  const size_t smem = MixSmem<DP, DU, Q, G::E>::BYTES;
+  if (mode == MIX_BOTH)
+    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true><<<blocks, G::T, smem, s>>>(tb, a);
+  else if (mode == MIX_TAU)
+    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false><<<blocks, G::T, smem, s>>>(tb, a);
+  else if (mode == MIX_VB)
+    mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true><<<blocks, G::T, smem, s>>>(tb, a);
+  else
+    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true>
+        <<<blocks, G::T, MixSmem<DP, DU, Q, G::E, true>::BYTES, s>>>(tb, a);
+}
+
+template <int P, int CFG>
+MixKernel mix_entry() {
+  constexpr int DP = P + 1, DU = P, Q = P + 1;
+  using G = MixGeom<DP, DU, Q, CFG>;
+  using L = MixLayout<DP, DU, Q>;
+  MixKernel k;
+  k.dp = DP;
+  k.du = DU;
+  k.q = Q;
+  k.cfg = CFG;
+  k.E = G::E;
+  k.T = G::T;
+  k.ps = L::PS;
+  k.gs = L::GS;
+  k.smem = MixSmem<DP, DU, Q, G::E>::BYTES;
+  k.smem_mf = MixSmem<DP, DU, Q, G::E, true>::BYTES;
+  k.f_both = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true>);
+  k.f_tau = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false>);
+  k.f_vb = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true>);
+  k.f_mf = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true>);
+  k.launch = &mix_launch<DP, DU, Q, CFG>;
+  return k;
+}
+
+template <int P>
+void mix_add(std::vector<MixKernel>& v) {
+  v.push_back(mix_entry<P, 0>());
+  v.push_back(mix_entry<P, 1>());
+  v.push_back(mix_entry<P, 2>());
+  v.push_back(mix_entry<P, 3>());
+}
+
+}  // namespace
+}  // namespace fk
+
+#define FK_MCAT2(a, b) a##b
+#define FK_MCAT(a, b) FK_MCAT2(a, b)
+
+void FK_MCAT(fk_mix_register_p, FK_MIX_P)(std::vector<fk::MixKernel>& out) { fk::mix_add<FK_MIX_P>(out); }
