@@ -135,7 +135,11 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
       prefetch_l2(pa + (size_t)e0 * G::PS, bytes);
     } else {
       mbar_expect_tx(bar_d, bytes);
+#ifdef FK_PA_NO_L2_HINT
       bulk_g2s(db, pa + (size_t)e0 * G::PS, bytes, bar_d);
+#else
+      bulk_g2s_hint(db, pa + (size_t)e0 * G::PS, bytes, bar_d, l2_policy_evict_first());
+#endif
     }
   };
   auto issue_x = [&](int b, int gslot, double* xdst) {
