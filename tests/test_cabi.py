@@ -58,6 +58,8 @@ def _desc(**kw):
     (dict(q=4), _lib.FK_EUNSUPPORTED, "num_quad_1d"),
     (dict(nz_local=3), _lib.FK_EINVAL, "do not match"),
     (dict(jac_det=0.0), _lib.FK_EINVAL, "Jacobian"),
+    # maximum size: int32 dof ids (the device E-restriction) cap a rank at < 2^31 dofs
+    (dict(nx=2300, ny=2300, nz_local=60, nz_global=60), _lib.FK_EINVAL, "too large"),
     (dict(variant=7), _lib.FK_EINVAL, "variant"),
 ])
 def test_descriptor_validation(kw, code, needle):
