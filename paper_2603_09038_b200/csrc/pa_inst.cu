@@ -3,8 +3,9 @@
 // compilations in parallel); each object exports fk_register_p<p>().
 //
 // Several launch geometries (elements per CTA E, threads T) are compiled per
-// (kind, p, q, variant); the first registered is the default, the others are
-// selectable (FK_CFG=<index>) for the tuning sweep recorded in DESIGN.md.
+// (kind, p, q, variant) and selectable by (variant, cfg) (fk_op_set_config,
+// FK_CFG) for the tuning sweeps recorded in DESIGN.md; FK_VARIANT_AUTO picks
+// the measured best per order (fk_api.cu kAutoVar*/kAutoCfg*).
 #include <cstring>
 
 #include "fk_internal.h"
@@ -83,8 +84,8 @@ void add_tuned_eo(std::vector<KernelEntry>& out, int c0) {
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, PP>, true>(FK_VARIANT_EO, c0 + 8));
 }
 
-// Compiled launch geometries (cfg index per variant; cfg 0 is the default).
-// Measured per order in the sweep (profiles/r01_sweep_*).
+// Compiled launch geometries (cfg index per variant), measured per order in
+// the sweeps (profiles/r01_sweep_*).
 template <int D, int Q, int NC>
 void add_all(std::vector<KernelEntry>& out) {
   constexpr int E0 = base_E(Q);
