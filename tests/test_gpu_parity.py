@@ -396,6 +396,20 @@ def test_matrix_free_strategy_matches_pa(strategy, kind):
         assert normwise(op.apply(dev(x)).cpu().numpy(), P.apply(x)) <= PARITY_TOL
 
 
+@pytest.mark.parametrize("qoff", [1, 2])
+@pytest.mark.parametrize("p", [1, 3, 5, 8])
+def test_matrix_free_anisotropic(p, qoff):
+    """MF on a non-cubic box (jinv differs per direction, D_ss = w|J| jinv_s^2)
+    and with q = p+1 and p+2, with Dirichlet bits."""
+    ext = (2.0, 1.0, 0.5)
+    n = (4, 3, 2) if p <= 4 else (2, 3, 2)
+    P = bp.Problem("diffusion", *n, p, p + qoff, extents=ext)
+    x = np.random.default_rng(p).standard_normal(P.ndof)
+    op = make("diffusion", n, p, p + qoff, ext, strategy="MF", dirichlet=True)
+    ref = P.constrained_apply(x, P.boundary())
+    assert normwise(op.apply(dev(x)).cpu().numpy(), ref) <= PARITY_TOL
+
+
 def test_reference_objects_drop_in(golden):
     """The operator consumes duck-typed mesh/basis objects (feklab's or ours)."""
     class RefLikeMesh:
