@@ -57,19 +57,14 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // The FP64-FMA line kernels win at every order on sm_100a: DMMA and DFMA share
 // the 37 TFLOP/s FP64 pipe, and DMMA's 8x8x4 padding wastes 14-88% of it at
 // these shapes.
-// (variant, cfg) per order, best of profiles/r01_sweep_v11_static_tables.jsonl
-// (tools/auto_table.py)
+// (variant, cfg) per order, best of profiles/r01_sweep_f3.jsonl + r01_sweep_v17_structured_ids.jsonl
+// (tools/auto_table.py); structured-id geometries (eo19-24) fall back to cfg 0
+// when the caller passes its own gather map
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg3[9] = {0, 14, 1, 11, 5, 1, 14, 18, 10};  // p=4: eo5, 3 repeated sweeps (r01_sweep_v15_p4_reps)
+const int kAutoCfg3[9] = {0, 14, 2, 2, 19, 2, 14, 18, 10};
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg1[9] = {0, 9, 6, 9, 2, 18, 10, 14, 14};
-
-int auto_variant(int nc, int p, int q) {
-  (void)q;
-  if (p < 1 || p > 8) return FK_VARIANT_DFMA;
-  return nc == 3 ? kAutoVar3[p] : kAutoVar1[p];
-}
+const int kAutoCfg1[9] = {0, 23, 24, 24, 23, 24, 23, 24, 24};
 
 // matrix-free geometry per order (best of profiles/r01_sweep_v14_mf.jsonl)
 const int kAutoCfgMF3[9] = {0, 7, 3, 5, 5, 5, 6, 5, 6};
@@ -95,6 +90,12 @@ fk::OpView view(const fk_op* op) {
   v.w = op->w;
   v.detj = op->desc.jac_det;
   for (int s = 0; s < 3; ++s) v.jinv[s] = op->jinv[s];
+  v.nx = op->desc.nx;
+  v.ny = op->desc.ny;
+  v.p = op->p;
+  v.npx = op->npx;
+  v.npy = op->npy;
+  v.e0 = 0;
   return v;
 }
 
@@ -125,6 +126,12 @@ int select_kernel(fk_op* op, int variant) {
   else if (variant == FK_VARIANT_AUTO) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, auto_cfg(op->nc, op->p));
   else if (variant == FK_VARIANT_MF) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, auto_cfg_mf(op->nc, op->p));
   if (k == nullptr) k = fk::find_kernel(op->nc, op->d, op->q, v);
+  if (k != nullptr && k->structured && !op->host_gids.empty()) {
+    if (op->cfg >= 0)
+      return fail(FK_EUNSUPPORTED, "launch config %d uses the closed-form box restriction; "
+                                   "a user gather map was given", op->cfg);
+    k = fk::find_kernel(op->nc, op->d, op->q, v);  // cfg 0: array map
+  }
   if (k == nullptr)
     return fail(FK_EUNSUPPORTED, "no %s kernel compiled for kind=%d p=%d q=%d",
                 v == FK_VARIANT_DMMA ? "DMMA" : v == FK_VARIANT_EO ? "even-odd" : v == FK_VARIANT_MF ? "matrix-free" : "DFMA",
@@ -179,6 +186,7 @@ int launch_range(fk_op* op, const double* x, double* y, int64_t e0, int64_t ne, 
   fk::OpView v = view(op);
   v.gids += e0 * op->gs;
   v.pa += e0 * op->ps;
+  v.e0 = e0;
   if (v.ebits) v.ebits += e0 * op->ms;
   v.nel = (int)ne;
   const int64_t nb = (ne + op->kern->E - 1) / op->kern->E;

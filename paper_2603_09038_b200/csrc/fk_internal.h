@@ -19,6 +19,7 @@ struct KernelEntry {
   int nc = 0, d = 0, q = 0, variant = 0, cfg = 0;
   int E = 0, T = 0;
   bool persist = true;  // persistent grid (batches strided over CTAs) or one batch per CTA
+  bool structured = false;  // ids from the closed-form box restriction (no user gather map)
   size_t smem = 0;
   const void* func = nullptr;
   LaunchFn launch = nullptr;
@@ -35,6 +36,10 @@ struct OpView {
   const double* w;  // host quadrature weights (q), |J| and 1/jac_diag: MF kernels
   double detj;
   double jinv[3];
+  // closed-form restriction (GM = 1 kernels): slab sizes and the first element
+  // of this launch within the rank's slab
+  int nx, ny, p;
+  int64_t npx, npy, e0;
 };
 
 // Host mirror of GlobalLayout (pa_common.cuh): padded per-element strides.

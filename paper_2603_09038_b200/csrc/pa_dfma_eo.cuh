@@ -402,6 +402,32 @@ struct DfmaEoBody {
     });
   }
 
+  // stage E with the ids from a functor gid(e, l) (closed-form restriction)
+  template <class GidF>
+  __device__ __forceinline__ static void stage_e_ids(const Tab& tb, int it, const double* sr, GidF gid,
+                                                     double* y, int ne, double*) {
+    const double* tab = tb.t[PP ? (it & 1) : 0];
+    lines<LP::ME, D, D>(ne, [&](int e, int j, int k) {
+      const int g0 = gid(e, D * (j + D * k));  // ids along a line are consecutive (i fastest)
+      double rv[Q], out[D];
+#pragma unroll
+      for (int a = 0; a < Q; ++a) rv[a] = sr[LR::at(e, 0, a, j, k)];
+      if constexpr (NC == 3) {
+        double o2[D];
+        contract_eo<Q, D, -1>(tab + Tab::TGT, rv, out);  // G^T rG
+#pragma unroll
+        for (int a = 0; a < Q; ++a) rv[a] = sr[LR::at(e, 1, a, j, k)];
+        contract_eo<Q, D, +1>(tab + Tab::TBT, rv, o2);  // B^T rB
+#pragma unroll
+        for (int i = 0; i < D; ++i) atomicAdd(y + g0 + i, out[i] + o2[i]);
+      } else {
+        contract_eo<Q, D, +1>(tab + Tab::TBT, rv, out);
+#pragma unroll
+        for (int i = 0; i < D; ++i) atomicAdd(y + g0 + i, out[i]);
+      }
+    });
+  }
+
   // R (a, j, k) -> y (atomic scatter-add): thread per line (j, k)
   __device__ __forceinline__ static void stage_e(const Tab& tb, int it, const double* sr,
                                                  const int* gslot, double* y, int ne, double*) {

@@ -27,14 +27,16 @@ constexpr int round32(int n) { return ((n + 31) / 32) * 32; }
 // stage C (q^2 lines per element) is the heaviest: E*q^2 lines ~ 288
 constexpr int base_E(int Q) { return (288 / (Q * Q)) > 0 ? (288 / (Q * Q)) : 1; }
 
-template <int D, int Q, int NC, class Body, bool PERSIST, bool DG, bool MF = false>
+template <int D, int Q, int NC, class Body, bool PERSIST, bool DG, bool MF = false, int GM = 0,
+          bool SX = false>
 void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
   typename Body::Tab tb;
   Body::fill(tb, v.B, v.G);
   if constexpr (MF) Body::fill_mf(tb, v.w, v.detj, v.jinv);
-  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF>
-      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body, DG || MF>::BYTES, s>>>(
-          tb, x, y, v.gids, v.pa, v.ebits, v.nel);
+  const StructIds sid{v.nx, v.ny, v.p, (int)v.npx, (int)v.npy, (long long)v.e0};
+  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX>
+      <<<blocks, Body::T, PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES, s>>>(
+          tb, x, y, v.gids, v.pa, v.ebits, v.nel, sid);
 }
 
 template <int D, int Q, int NC>
@@ -45,7 +47,8 @@ void launch_diag(const OpView& v, double* diag, int64_t nel, int blocks, cudaStr
   diagonal_kernel<D, Q, NC><<<blocks, 128, 0, s>>>(tb, diag, v.gids, v.pa, nel);
 }
 
-template <int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false, bool MF = false>
+template <int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false, bool MF = false,
+          int GM = 0, bool SX = false>
 KernelEntry entry(int variant, int cfg) {
   KernelEntry k;
   k.nc = NC;
@@ -56,9 +59,10 @@ KernelEntry entry(int variant, int cfg) {
   k.E = Body::E;
   k.T = Body::T;
   k.persist = PERSIST;
-  k.smem = PipeSmem<D, Q, NC, Body, DG || MF>::BYTES;
-  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF>);
-  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF>;
+  k.structured = GM == 1;
+  k.smem = PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES;
+  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX>);
+  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX>;
   k.diag = &launch_diag<D, Q, NC>;
   return k;
 }
@@ -113,6 +117,14 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, O2, true>(FK_VARIANT_EO, 0));
   add_tuned_eo<D, Q, NC, true>(out, 1);
   add_tuned_eo<D, Q, NC, false>(out, 10);
+  // closed-form restriction (no id traffic, 1 int per element per slot) with a
+  // single X buffer: less smem per CTA -> more CTAs per SM
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, true>(FK_VARIANT_EO, 19));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, true>, true, false, false, 1, true>(FK_VARIANT_EO, 20));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, false>(FK_VARIANT_EO, 21));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, false>, true, false, false, 1, true>(FK_VARIANT_EO, 22));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, false>, true, false, false, 1, true>(FK_VARIANT_EO, 23));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true>(FK_VARIANT_EO, 24));
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;
   using M1 = TunedEo<D, Q, NC, E1, false, true>;

@@ -51,22 +51,33 @@ struct XAddr<D, Q, NC, Body, true> {
   __device__ __forceinline__ static void map(int t, int& e, int& l) { Body::gather_map(t, e, l); }
 };
 
-template <int D, int Q, int NC, class Body, bool DG = false>
+// Closed-form element restriction of the structured box (h1_restriction,
+// mesh.py:157-164) for the GM = 1 kernels: the id of node (i, j, k) of local
+// element e is base(e) + i + npx (j + npy k), base(e) = ex p + npx (ey p +
+// npy ez p).  e0 = first element of this launch within the rank's slab.
+struct StructIds {
+  int nx, ny, p, npx, npy;
+  long long e0;
+};
+
+template <int D, int Q, int NC, class Body, bool DG = false, int GM = 0, bool SX = false>
 struct PipeSmem {
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
   static constexpr int E = Body::E, EXTRA = Body::EXTRA;
   static constexpr int XS = XAddr<D, Q, NC, Body>::XS;  // X buffer doubles per element
   static constexpr int NG = 3;              // gather-id slots (batches b, b+1, b+2)
+  static constexpr int GSS = GM == 1 ? 1 : G::GS;  // ints per element in a slot (GM 1: base id)
+  static constexpr int NX = SX ? 1 : 2;             // X buffers
   // byte offsets (16-byte aligned where bulk copies land)
   static constexpr size_t OFF_BAR = 0;                                 // 4 mbarriers
   static constexpr size_t OFF_DB = 32;                                 // PA data
   static constexpr size_t OFF_GS = OFF_DB + (DG ? 0ull : 8ull * E * G::PS);  // NG gid slots
-  static constexpr size_t OFF_MS = OFF_GS + 4ull * NG * E * G::GS;     // NG bit slots
+  static constexpr size_t OFF_MS = OFF_GS + (4ull * NG * E * GSS + 15) / 16 * 16;  // NG bit slots
   static constexpr size_t OFF_S0 = OFF_MS + 4ull * NG * E * G::MS;
   static constexpr size_t OFF_S1 = OFF_S0 + 8ull * E * Body::P0;
   static constexpr size_t OFF_XB = OFF_S1 + 8ull * E * Body::P1;      // 2 X buffers
-  static constexpr size_t OFF_EX = (OFF_XB + 8ull * 2 * E * XS + 15) / 16 * 16;
+  static constexpr size_t OFF_EX = (OFF_XB + 8ull * NX * E * XS + 15) / 16 * 16;
   static constexpr size_t BYTES = OFF_EX + 8ull * EXTRA;
 };
 
@@ -75,18 +86,23 @@ struct PipeSmem {
 // toward L2 with cp.async.bulk.prefetch.L2 instead of copied into smem.
 // MF (matrix-free, even-odd bodies only): no PA data at all — stage C
 // recomputes D from the 1D weights and the element Jacobian (Body::stage_c<true>).
-template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false, bool MF = false>
+// GM = 1 (even-odd bodies): gather ids from the closed form (StructIds) —
+// no id array traffic, one int per element per slot.  SX: a single X buffer;
+// the next batch's gather is issued after stage A has consumed the current one.
+template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false, bool MF = false, int GM = 0,
+          bool SX = false>
 __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ typename Body::Tab tb,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
                                                           const int* __restrict__ gids,
                                                           const double* __restrict__ pa,
                                                           const uint32_t* __restrict__ ebits,
-                                                          int nel) {
+                                                          int nel, const StructIds sid) {
   constexpr int E = Body::E, T = Body::T;
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
-  using S = PipeSmem<D, Q, NC, Body, DG || MF>;
+  using S = PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>;
+  constexpr int GSS = S::GSS;
   using XA = XAddr<D, Q, NC, Body>;
   constexpr int D3 = L::D3, XS = S::XS, NG = S::NG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -120,12 +136,44 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   Body::init(tb, ex);
   __syncthreads();
 
+  // (thread 0) ids of batch b into slot: bulk copy of the id rows (GM 0) or
+  // the per-element base ids (GM 1), plus the Dirichlet bits
   auto issue_g = [&](int b, int slot) {
     const int e0 = b * E, ne = min(E, nel - e0);
-    const uint32_t gb = 4u * ne * G::GS, mb = dirichlet ? 4u * ne * G::MS : 0u;
-    mbar_expect_tx(bar_g + slot, gb + mb);
-    bulk_g2s(gs + slot * E * G::GS, gids + (size_t)e0 * G::GS, gb, bar_g + slot);
-    if (dirichlet) bulk_g2s(ms + slot * E * G::MS, ebits + (size_t)e0 * G::MS, mb, bar_g + slot);
+    if constexpr (GM == 1) {
+      (void)ne;
+      if (dirichlet) {
+        const uint32_t mb = 4u * ne * G::MS;
+        mbar_expect_tx(bar_g + slot, mb);
+        bulk_g2s(ms + slot * E * G::MS, ebits + (size_t)e0 * G::MS, mb, bar_g + slot);
+      }
+    } else {
+      const uint32_t gb = 4u * ne * G::GS, mb = dirichlet ? 4u * ne * G::MS : 0u;
+      mbar_expect_tx(bar_g + slot, gb + mb);
+      bulk_g2s(gs + slot * E * G::GS, gids + (size_t)e0 * G::GS, gb, bar_g + slot);
+      if (dirichlet) bulk_g2s(ms + slot * E * G::MS, ebits + (size_t)e0 * G::MS, mb, bar_g + slot);
+    }
+  };
+  // GM 1: base ids of batch b's elements into `slot`, one thread per element
+  // (all threads call this; visible to the CTA after the next barrier)
+  auto fill_base = [&](int b, int slot) {
+    if constexpr (GM == 1) {
+      const int e0 = b * E, ne = min(E, nel - e0);
+      for (int e = threadIdx.x; e < ne; e += T) {
+        const int eg = (int)(sid.e0 + e0 + e);  // local element counts are < 2^31
+        const int ex_ = eg % sid.nx, eyz = eg / sid.nx, ey_ = eyz % sid.ny, ez_ = eyz / sid.ny;
+        gs[slot * E + e] = ex_ * sid.p + sid.npx * (ey_ * sid.p + sid.npy * (ez_ * sid.p));
+      }
+    }
+  };
+  // global id of local node l of element e in gid slot `slot`
+  auto gid_of = [&](int slot, int e, int l) -> int {
+    if constexpr (GM == 1) {
+      const int k = l / (D * D), j = (l / D) % D, i = l - D * (j + D * k);
+      return gs[slot * E + e] + i + sid.npx * (j + sid.npy * k);
+    } else {
+      return gs[slot * E * G::GS + e * G::GS + l];
+    }
   };
   auto issue_d = [&](int b) {
     if constexpr (MF) return;
@@ -144,12 +192,11 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   };
   auto issue_x = [&](int b, int gslot, double* xdst) {
     const int e0 = b * E, ne = min(E, nel - e0);
-    const int* g = gs + gslot * E * G::GS;
     for (int t = threadIdx.x; t < E * D3; t += T) {
       int e, l;
       XA::map(t, e, l);
       double* dst = xdst + XA::off(e, l);
-      if (e < ne) cp_async8(dst, x + g[e * G::GS + l]);
+      if (e < ne) cp_async8(dst, x + gid_of(gslot, e, l));
       else *dst = 0.0;
     }
     cp_async_commit();
@@ -170,6 +217,7 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   // mbarrier phase bits of the gid slots (bit s) and of the D barrier
   uint32_t ph_g = 0u, ph_d = 0u;
   auto wait_g = [&](int slot) {
+    if (GM == 1 && !dirichlet) return;  // base ids are plain smem stores (ordered by barriers)
     mbar_wait(bar_g + slot, (ph_g >> slot) & 1u);
     ph_g ^= 1u << slot;
   };
@@ -181,27 +229,41 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     if (blockIdx.x + stride < nbatch) issue_g(blockIdx.x + stride, 1);
     issue_d(blockIdx.x);
   }
+  if constexpr (GM == 1) {  // base ids of the first two batches
+    fill_base(blockIdx.x, 0);
+    if (blockIdx.x + stride < nbatch) fill_base(blockIdx.x + stride, 1);
+    __syncthreads();
+  }
   wait_g(0);
   issue_x(blockIdx.x, 0, xb);
 
   auto run_batch = [&](int b, int it) {
     const int gslot = it % NG;
-    double* xcur = xb + (it & 1) * E * XS;
-    double* xnext = xb + ((it + 1) & 1) * E * XS;
+    double* xcur = SX ? xb : xb + (it & 1) * E * XS;
+    double* xnext = SX ? xb : xb + ((it + 1) & 1) * E * XS;
     const int e0 = b * E, ne = min(E, nel - e0);
     const int nb = b + stride, nb2 = nb + stride;
     finish_x(gslot, ne, xcur);
     __syncthreads();
     if (nb < nbatch) {
-      wait_g((it + 1) % NG);
-      issue_x(nb, (it + 1) % NG, xnext);
+      if constexpr (!SX) {
+        wait_g((it + 1) % NG);
+        issue_x(nb, (it + 1) % NG, xnext);
+      }
       if (nb2 < nbatch && threadIdx.x == 0) {
         fence_proxy_async();
         issue_g(nb2, (it + 2) % NG);  // slot last read by batch b-1 (done)
       }
+      if (nb2 < nbatch) fill_base(nb2, (it + 2) % NG);
     }
     Body::stage_a(tb, it, xcur, s1, ne, ex);
     __syncthreads();
+    if constexpr (SX) {  // X(b) consumed: gather X(b+1) into the same buffer
+      if (nb < nbatch) {
+        wait_g((it + 1) % NG);
+        issue_x(nb, (it + 1) % NG, xnext);
+      }
+    }
     Body::stage_b(tb, it, s1, s0, ne, ex);
     __syncthreads();
     if constexpr (MF) {
@@ -220,7 +282,11 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     }
     Body::stage_d(tb, it, sw, sr, ne, ex);
     __syncthreads();
-    Body::stage_e(tb, it, sr, gs + gslot * E * G::GS, y, ne, ex);
+    if constexpr (GM == 1) {
+      Body::stage_e_ids(tb, it, sr, [&](int e, int l) { return gid_of(gslot, e, l); }, y, ne, ex);
+    } else {
+      Body::stage_e(tb, it, sr, gs + gslot * E * G::GS, y, ne, ex);
+    }
     // no barrier here: every thread passes the barrier after the next batch's
     // finish_x only after its own stage E, and nothing before that barrier
     // touches the regions stage E reads (R, this batch's gid slot)

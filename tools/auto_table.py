@@ -7,6 +7,7 @@ import json
 import sys
 
 rows = [json.loads(l) for l in open(sys.argv[1])]
+rows = [r for r in rows if r["variant"] != "mf"]  # the PA table (MF has its own, kAutoCfgMF*)
 code = {"dfma": "D_", "dmma": "M_", "eo": "O_"}
 for kind, nc in (("diffusion", 3), ("mass", 1)):
     var, cfg = ["D_"], [0]
