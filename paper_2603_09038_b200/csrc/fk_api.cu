@@ -66,6 +66,12 @@ const int kAutoCfg3[9] = {0, 14, 2, 2, 19, 2, 14, 18, 10};
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
 const int kAutoCfg1[9] = {0, 23, 24, 24, 23, 24, 23, 24, 24};
 
+int auto_variant(int nc, int p, int q) {
+  (void)q;
+  if (p < 1 || p > 8) return FK_VARIANT_DFMA;
+  return nc == 3 ? kAutoVar3[p] : kAutoVar1[p];
+}
+
 // matrix-free geometry per order (best of profiles/r01_sweep_v14_mf.jsonl)
 const int kAutoCfgMF3[9] = {0, 7, 3, 5, 5, 5, 6, 5, 6};
 const int kAutoCfgMF1[9] = {0, 3, 3, 3, 4, 5, 4, 4, 4};
