@@ -20,6 +20,7 @@ from .fem import (
     h1_node_coords,
     h1_restriction,
 )
+from . import mapping
 from .mixed import MixedOperator, rk4_step
 from .mixed import State as MixedState
 from .operator import (
@@ -39,5 +40,5 @@ __all__ = [
     "PAData", "PAOperator", "rk4_step",
     "Restriction", "ShapeError", "boundary_dofs", "build_mesh", "bytes_per_apply",
     "cg_solve", "flops_per_element", "gauss_points", "gll_points", "h1_gather_ids",
-    "h1_node_coords", "h1_restriction", "setup_pa_data", "__version__",
+    "h1_node_coords", "h1_restriction", "mapping", "setup_pa_data", "__version__",
 ]
