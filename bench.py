@@ -375,7 +375,8 @@ def run_ours(a):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src, "kernel_ms": ms_kernel,
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel": "fk::pa_dfma_kernel / pa_dmma_kernel (fused gather-B/G-D-B^T/G^T-scatter)"},
+                         "kernel": f"fused apply kernel, variant {op.variant} (pa_pipe_kernel: gather, B/G, D, "
+                                   "B^T/G^T, scatter-add in one launch)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * op.num_dofs,
                     "d2h_bytes_per_step": 8 * op.num_dofs, "ms_per_step": e2e_ms,
