@@ -408,7 +408,7 @@ struct DfmaEoBody {
                                                      double* y, int ne, double*) {
     const double* tab = tb.t[PP ? (it & 1) : 0];
     lines<LP::ME, D, D>(ne, [&](int e, int j, int k) {
-      const int g0 = gid(e, D * (j + D * k));  // ids along a line are consecutive (i fastest)
+      const int g0 = gid(e, j, k);  // id of node (0, j, k); ids along a line are consecutive
       double rv[Q], out[D];
 #pragma unroll
       for (int a = 0; a < Q; ++a) rv[a] = sr[LR::at(e, 0, a, j, k)];

@@ -27,14 +27,31 @@ constexpr int round32(int n) { return ((n + 31) / 32) * 32; }
 // stage C (q^2 lines per element) is the heaviest: E*q^2 lines ~ 288
 constexpr int base_E(int Q) { return (288 / (Q * Q)) > 0 ? (288 / (Q * Q)) : 1; }
 
+// round-up multiplier for n / d = (umulhi(n, m) + n) >> s, exact for n < 2^31
+// (Granlund-Montgomery; pa_pipe.cuh fast_div)
+void div_magic(int d, unsigned& m, int& s) {
+  s = 0;
+  while ((1ll << s) < d) ++s;
+  m = (unsigned)((((1ull << 32) * ((1ull << s) - (unsigned long long)d)) / (unsigned long long)d) + 1);
+}
+
+StructIds struct_ids(const OpView& v) {
+  StructIds sid{v.nx, v.ny, v.p, (int)v.npx, (int)v.npy, (long long)v.e0, 0u, 0u, 0, 0};
+  if (v.nx > 0 && v.ny > 0) {
+    div_magic(v.nx, sid.mnx, sid.snx);
+    div_magic(v.ny, sid.mny, sid.sny);
+  }
+  return sid;
+}
+
 template <int D, int Q, int NC, class Body, bool PERSIST, bool DG, bool MF = false, int GM = 0,
-          bool SX = false>
+          bool SX = false, bool XP = false>
 void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
   typename Body::Tab tb;
   Body::fill(tb, v.B, v.G);
   if constexpr (MF) Body::fill_mf(tb, v.w, v.detj, v.jinv);
-  const StructIds sid{v.nx, v.ny, v.p, (int)v.npx, (int)v.npy, (long long)v.e0};
-  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX>
+  const StructIds sid = struct_ids(v);
+  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>
       <<<blocks, Body::T, PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES, s>>>(
           tb, x, y, v.gids, v.pa, v.ebits, v.nel, sid);
 }
@@ -48,7 +65,7 @@ void launch_diag(const OpView& v, double* diag, int64_t nel, int blocks, cudaStr
 }
 
 template <int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false, bool MF = false,
-          int GM = 0, bool SX = false>
+          int GM = 0, bool SX = false, bool XP = false>
 KernelEntry entry(int variant, int cfg) {
   KernelEntry k;
   k.nc = NC;
@@ -61,8 +78,8 @@ KernelEntry entry(int variant, int cfg) {
   k.persist = PERSIST;
   k.structured = GM == 1;
   k.smem = PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES;
-  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX>);
-  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX>;
+  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>);
+  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>;
   k.diag = &launch_diag<D, Q, NC>;
   return k;
 }
@@ -125,6 +142,14 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, false>, true, false, false, 1, true>(FK_VARIANT_EO, 22));
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, false>, true, false, false, 1, true>(FK_VARIANT_EO, 23));
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true>(FK_VARIANT_EO, 24));
+  // cfgs 25-31: cfgs 2, 10, 14, 18, 19, 23, 24 with the gather slots precomputed (XP)
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, true>, true, false, false, 0, false, true>(FK_VARIANT_EO, 25));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, false>, true, false, false, 0, false, true>(FK_VARIANT_EO, 26));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, false>, true, false, false, 0, false, true>(FK_VARIANT_EO, 27));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 0, false, true>(FK_VARIANT_EO, 28));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, true, true>(FK_VARIANT_EO, 29));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 30));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 31));
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;
   using M1 = TunedEo<D, Q, NC, E1, false, true>;

@@ -55,10 +55,18 @@ struct XAddr<D, Q, NC, Body, true> {
 // mesh.py:157-164) for the GM = 1 kernels: the id of node (i, j, k) of local
 // element e is base(e) + i + npx (j + npy k), base(e) = ex p + npx (ey p +
 // npy ez p).  e0 = first element of this launch within the rank's slab.
+// mnx/snx, mny/sny: division by nx and ny as (umulhi(n, m) + n) >> s
+// (round-up multiplier, exact for n < 2^31; host side struct_ids, pa_inst.cu).
 struct StructIds {
   int nx, ny, p, npx, npy;
   long long e0;
+  unsigned mnx, mny;
+  int snx, sny;
 };
+
+__device__ __forceinline__ int fast_div(int n, unsigned m, int s) {
+  return (int)((__umulhi((unsigned)n, m) + (unsigned)n) >> s);
+}
 
 template <int D, int Q, int NC, class Body, bool DG = false, int GM = 0, bool SX = false>
 struct PipeSmem {
@@ -90,7 +98,7 @@ struct PipeSmem {
 // no id array traffic, one int per element per slot.  SX: a single X buffer;
 // the next batch's gather is issued after stage A has consumed the current one.
 template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false, bool MF = false, int GM = 0,
-          bool SX = false>
+          bool SX = false, bool XP = false>
 __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ typename Body::Tab tb,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
@@ -161,7 +169,8 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
       const int e0 = b * E, ne = min(E, nel - e0);
       for (int e = threadIdx.x; e < ne; e += T) {
         const int eg = (int)(sid.e0 + e0 + e);  // local element counts are < 2^31
-        const int ex_ = eg % sid.nx, eyz = eg / sid.nx, ey_ = eyz % sid.ny, ez_ = eyz / sid.ny;
+        const int eyz = fast_div(eg, sid.mnx, sid.snx), ez_ = fast_div(eyz, sid.mny, sid.sny);
+        const int ex_ = eg - eyz * sid.nx, ey_ = eyz - ez_ * sid.ny;
         gs[slot * E + e] = ex_ * sid.p + sid.npx * (ey_ * sid.p + sid.npy * (ez_ * sid.p));
       }
     }
@@ -190,14 +199,54 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
 #endif
     }
   };
+  // XP: this thread's gather slots are the same in every batch, so their
+  // X-buffer offsets, (element << 16 | node) and id offsets (GM 1: relative
+  // to the element's base id, GM 0: into the slot's id rows) are computed once
+  // here instead of per batch — the index arithmetic is ~20% of BP1's
+  // instructions, but the extra live registers change ptxas' allocation of
+  // the basis tables, so it is a per-geometry choice (cfgs 25-31, pa_inst.cu).
+  constexpr int NXT = (E * D3 + T - 1) / T;
+  constexpr bool XPRE = XP && NXT <= 8;
+  int x_off[XPRE ? NXT : 1], x_el[XPRE ? NXT : 1], x_rel[XPRE ? NXT : 1];
+  if constexpr (XPRE) {
+#pragma unroll
+    for (int r = 0; r < NXT; ++r) {
+      const int t = threadIdx.x + r * T;
+      int e = E, l = 0;
+      if (t < E * D3) XA::map(t, e, l);
+      x_off[r] = t < E * D3 ? XA::off(e, l) : 0;
+      x_el[r] = (e << 16) | l;
+      if constexpr (GM == 1) {
+        const int k = l / (D * D), j = (l / D) % D, i = l - D * (j + D * k);
+        x_rel[r] = i + sid.npx * (j + sid.npy * k);
+      } else {
+        x_rel[r] = e * G::GS + l;
+      }
+    }
+  }
   auto issue_x = [&](int b, int gslot, double* xdst) {
     const int e0 = b * E, ne = min(E, nel - e0);
-    for (int t = threadIdx.x; t < E * D3; t += T) {
-      int e, l;
-      XA::map(t, e, l);
-      double* dst = xdst + XA::off(e, l);
-      if (e < ne) cp_async8(dst, x + gid_of(gslot, e, l));
-      else *dst = 0.0;
+    if constexpr (XPRE) {
+#pragma unroll
+      for (int r = 0; r < NXT; ++r) {
+        const int e = x_el[r] >> 16;
+        if (e >= E) continue;  // past the batch's E * D^3 slots
+        double* dst = xdst + x_off[r];
+        if (e < ne) {
+          const int g = GM == 1 ? gs[gslot * E + e] + x_rel[r] : gs[gslot * E * G::GS + x_rel[r]];
+          cp_async8(dst, x + g);
+        } else {
+          *dst = 0.0;
+        }
+      }
+    } else {
+      for (int t = threadIdx.x; t < E * D3; t += T) {
+        int e, l;
+        XA::map(t, e, l);
+        double* dst = xdst + XA::off(e, l);
+        if (e < ne) cp_async8(dst, x + gid_of(gslot, e, l));
+        else *dst = 0.0;
+      }
     }
     cp_async_commit();
   };
@@ -207,10 +256,18 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
       const uint32_t* m = ms + gslot * E * G::MS;
       // same thread -> (e, l) map as issue_x: cp.async.wait_group only covers
       // this thread's own copies
-      for (int t = threadIdx.x; t < E * D3; t += T) {
-        int e, l;
-        XA::map(t, e, l);
-        if (e < ne && ((m[e * G::MS + (l >> 5)] >> (l & 31)) & 1u)) xsrc[XA::off(e, l)] = 0.0;
+      if constexpr (XPRE) {
+#pragma unroll
+        for (int r = 0; r < NXT; ++r) {
+          const int e = x_el[r] >> 16, l = x_el[r] & 0xffff;
+          if (e < ne && ((m[e * G::MS + (l >> 5)] >> (l & 31)) & 1u)) xsrc[x_off[r]] = 0.0;
+        }
+      } else {
+        for (int t = threadIdx.x; t < E * D3; t += T) {
+          int e, l;
+          XA::map(t, e, l);
+          if (e < ne && ((m[e * G::MS + (l >> 5)] >> (l & 31)) & 1u)) xsrc[XA::off(e, l)] = 0.0;
+        }
       }
     }
   };
@@ -283,7 +340,9 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     Body::stage_d(tb, it, sw, sr, ne, ex);
     __syncthreads();
     if constexpr (GM == 1) {
-      Body::stage_e_ids(tb, it, sr, [&](int e, int l) { return gid_of(gslot, e, l); }, y, ne, ex);
+      Body::stage_e_ids(
+          tb, it, sr, [&](int e, int j, int k) { return gs[gslot * E + e] + sid.npx * (j + sid.npy * k); },
+          y, ne, ex);
     } else {
       Body::stage_e(tb, it, sr, gs + gslot * E * G::GS, y, ne, ex);
     }
