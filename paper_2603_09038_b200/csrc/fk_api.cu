@@ -73,9 +73,10 @@ int auto_variant(int nc, int p, int q) {
   return nc == 3 ? kAutoVar3[p] : kAutoVar1[p];
 }
 
-// matrix-free geometry per order (best of profiles/r01_sweep_v14_mf.jsonl)
+// matrix-free geometry per order (best of profiles/r01_sweep_v14_mf.jsonl; BP1
+// p=2/3 from r01_sweep_v20_mf_xp.jsonl, +8%/+5%)
 const int kAutoCfgMF3[9] = {0, 7, 3, 5, 5, 5, 6, 5, 6};
-const int kAutoCfgMF1[9] = {0, 3, 3, 3, 4, 5, 4, 4, 4};
+const int kAutoCfgMF1[9] = {0, 3, 9, 8, 4, 5, 4, 4, 4};
 int auto_cfg_mf(int nc, int p) {
   if (p < 1 || p > 8) return 0;
   return nc == 3 ? kAutoCfgMF3[p] : kAutoCfgMF1[p];

@@ -167,6 +167,11 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, M1s, true, false, true>(FK_VARIANT_MF, 5));
   out.push_back(entry<D, Q, NC, M2is, true, false, true>(FK_VARIANT_MF, 6));
   out.push_back(entry<D, Q, NC, M0is, true, false, true>(FK_VARIANT_MF, 7));
+  // mf8-9: closed-form ids (GM 1) and precomputed gather slots (XP); with the
+  // static-table three-component bodies XP costs registers, so BP1 only gains
+  // (profiles/r01_sweep_v20_mf_xp.jsonl)
+  out.push_back(entry<D, Q, NC, M1s, true, false, true, 1, false, true>(FK_VARIANT_MF, 8));
+  out.push_back(entry<D, Q, NC, M0is, true, false, true, 1, false, true>(FK_VARIANT_MF, 9));
 }
 
 }  // namespace
