@@ -57,13 +57,15 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // The FP64-FMA line kernels win at every order on sm_100a: DMMA and DFMA share
 // the 37 TFLOP/s FP64 pipe, and DMMA's 8x8x4 padding wastes 14-88% of it at
 // these shapes.
-// (variant, cfg) per order, best of profiles/r01_sweep_v19_xp.jsonl (one box,
-// every candidate geometry incl. the precomputed-gather cfgs 25-31;
-// tools/auto_table.py); structured-id geometries (eo19-24, 29-31) fall back
-// to cfg 0 when the caller passes its own gather map
+// (variant, cfg) per order, best of profiles/r01_sweep_v21_shared_rows.jsonl
+// (BP3; one box, every candidate geometry incl. the precomputed-gather cfgs
+// 25-31, shared table rows) and r01_sweep_v19_xp.jsonl (BP1); BP3 p=4 from
+// the repeated A/B r01_ab_p4_cfg29_32.log (cfg 32 = 29 without shared rows,
+// +1.5%); tools/auto_table.py.  Structured-id geometries (eo19-24, 29-32)
+// fall back to cfg 0 when the caller passes its own gather map
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg3[9] = {0, 19, 2, 2, 29, 25, 14, 18, 23};
+const int kAutoCfg3[9] = {0, 19, 2, 2, 32, 25, 14, 18, 23};
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
 const int kAutoCfg1[9] = {0, 18, 31, 31, 30, 23, 30, 23, 29};
 

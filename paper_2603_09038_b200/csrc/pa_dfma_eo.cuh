@@ -71,6 +71,43 @@ inline void fold_table(double* dst, const double* N, int S) {
   }
 }
 
+// one folded row applied to a folded input: E (even part, + middle entry) and O
+template <int NI, int RL, int HI>
+__device__ __forceinline__ void eo_row(const double (&row)[RL], const double* xe, const double* xo,
+                                       double mid, double& E, double& O) {
+  if constexpr (NI & 1) {
+    E = row[2 * HI] * mid;
+#pragma unroll
+    for (int i = 0; i < HI; ++i) E = fma(row[i], xe[i], E);
+  } else {
+    E = row[0] * xe[0];
+#pragma unroll
+    for (int i = 1; i < HI; ++i) E = fma(row[i], xe[i], E);
+  }
+  if constexpr (HI > 0) {
+    O = row[HI] * xo[0];
+#pragma unroll
+    for (int i = 1; i < HI; ++i) O = fma(row[HI + i], xo[i], O);
+  } else {
+    O = 0.0;
+  }
+}
+
+template <int NI>
+__device__ __forceinline__ void eo_fold(const double (&in)[NI], double* xe, double* xo) {
+#pragma unroll
+  for (int i = 0; i < NI / 2; ++i) {
+    xe[i] = in[i] + in[NI - 1 - i];
+    xo[i] = in[i] - in[NI - 1 - i];
+  }
+}
+
+template <int NO, int S>
+__device__ __forceinline__ void eo_out(int a, double E, double O, double (&out)[NO]) {
+  out[a] = E + O;
+  if (a != NO - 1 - a) out[NO - 1 - a] = (S > 0) ? (E - O) : (O - E);
+}
+
 // out = N in, N given folded at t (Fold<NO,NI> layout), symmetry sign S
 template <int NI, int NO, int S>
 __device__ __forceinline__ void contract_eo(const double* __restrict__ t, const double (&in)[NI],
@@ -78,38 +115,50 @@ __device__ __forceinline__ void contract_eo(const double* __restrict__ t, const 
   using F = Fold<NO, NI>;
   constexpr int HI = F::HI;
   double xe[HI > 0 ? HI : 1], xo[HI > 0 ? HI : 1];
-#pragma unroll
-  for (int i = 0; i < HI; ++i) {
-    xe[i] = in[i] + in[NI - 1 - i];
-    xo[i] = in[i] - in[NI - 1 - i];
-  }
+  eo_fold<NI>(in, xe, xo);
 #pragma unroll
   for (int a = 0; a < F::HO; ++a) {
     double row[F::RL];
     ld_row(t + a * F::RP, row);
     double E, O;
-    if constexpr (NI & 1) {
-      E = row[2 * HI] * in[HI];
+    eo_row<NI, F::RL, HI>(row, xe, xo, in[HI], E, O);
+    eo_out<NO, S>(a, E, O, out);
+  }
+}
+
+// the same table applied to two inputs: every folded row is loaded once
+// (LDCU.128 table loads were ~18% of the BP3 kernel's instructions)
+template <int NI, int NO, int S>
+__device__ __forceinline__ void contract_eo2(const double* __restrict__ t, const double (&in0)[NI],
+                                             const double (&in1)[NI], double (&out0)[NO],
+                                             double (&out1)[NO]) {
+  using F = Fold<NO, NI>;
+  constexpr int HI = F::HI;
+  double xe0[HI > 0 ? HI : 1], xo0[HI > 0 ? HI : 1], xe1[HI > 0 ? HI : 1], xo1[HI > 0 ? HI : 1];
+  eo_fold<NI>(in0, xe0, xo0);
+  eo_fold<NI>(in1, xe1, xo1);
 #pragma unroll
-      for (int i = 0; i < HI; ++i) E = fma(row[i], xe[i], E);
-    } else {
-      E = row[0] * xe[0];
-#pragma unroll
-      for (int i = 1; i < HI; ++i) E = fma(row[i], xe[i], E);
-    }
-    if constexpr (HI > 0) {
-      O = row[HI] * xo[0];
-#pragma unroll
-      for (int i = 1; i < HI; ++i) O = fma(row[HI + i], xo[i], O);
-    } else {
-      O = 0.0;
-    }
-    if (a == NO - 1 - a) {
-      out[a] = E + O;
-    } else {
-      out[a] = E + O;
-      out[NO - 1 - a] = (S > 0) ? (E - O) : (O - E);
-    }
+  for (int a = 0; a < F::HO; ++a) {
+    double row[F::RL];
+    ld_row(t + a * F::RP, row);
+    double E, O;
+    eo_row<NI, F::RL, HI>(row, xe0, xo0, in0[HI], E, O);
+    eo_out<NO, S>(a, E, O, out0);
+    eo_row<NI, F::RL, HI>(row, xe1, xo1, in1[HI], E, O);
+    eo_out<NO, S>(a, E, O, out1);
+  }
+}
+
+// two inputs through one table: shared row loads (SR) or two separate passes
+template <bool SR, int NI, int NO, int S>
+__device__ __forceinline__ void contract_pair(const double* __restrict__ t, const double (&in0)[NI],
+                                              const double (&in1)[NI], double (&out0)[NO],
+                                              double (&out1)[NO]) {
+  if constexpr (SR) {
+    contract_eo2<NI, NO, S>(t, in0, in1, out0, out1);
+  } else {
+    contract_eo<NI, NO, S>(t, in0, out0);
+    contract_eo<NI, NO, S>(t, in1, out1);
   }
 }
 
@@ -184,7 +233,7 @@ struct EoLayDefault {
 // (spilled) registers.  At p >= 6 with three components the dynamic index
 // instead makes ptxas fall back from uniform LDCU to per-thread LDC and holds
 // 126-165 registers (vs 75-88 static); PP = false uses the static copy 0.
-template <int D, int Q, int NC, int E_, int T_, class LP, bool PP = true>
+template <int D, int Q, int NC, int E_, int T_, class LP, bool PP = true, bool SR = true>
 struct DfmaEoBody {
   using L = LineLayout<D, Q, NC>;
   using G = GlobalLayout<D, Q, NC>;
@@ -291,15 +340,15 @@ struct DfmaEoBody {
         double gx[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) gx[j] = s1[LT1::at(e, 1, a, j, k)];
-        contract_eo<D, Q, +1>(tab + Tab::TB, gx, c);  // comp0 = B_y G_x
+        double c2[Q];
+        contract_pair<SR, D, Q, +1>(tab + Tab::TB, gx, bx, c, c2);  // comp0 = B_y G_x, comp2 = B_y B_x
 #pragma unroll
         for (int b = 0; b < Q; ++b) s0[LT2::at(e, 0, a, b, k)] = c[b];
+#pragma unroll
+        for (int b = 0; b < Q; ++b) s0[LT2::at(e, 2, a, b, k)] = c2[b];
         contract_eo<D, Q, -1>(tab + Tab::TG, bx, c);  // comp1 = G_y B_x
 #pragma unroll
         for (int b = 0; b < Q; ++b) s0[LT2::at(e, 1, a, b, k)] = c[b];
-        contract_eo<D, Q, +1>(tab + Tab::TB, bx, c);  // comp2 = B_y B_x
-#pragma unroll
-        for (int b = 0; b < Q; ++b) s0[LT2::at(e, 2, a, b, k)] = c[b];
       } else {
         contract_eo<D, Q, +1>(tab + Tab::TB, bx, c);
 #pragma unroll
@@ -335,8 +384,7 @@ struct DfmaEoBody {
       const double wab = MF ? tb.mfw[b] * tb.mfw[a] : 0.0;
       if constexpr (NC == 3) {
         double g0[Q], g1[Q], g2[Q];
-        contract_eo<D, Q, +1>(tab + Tab::TB, tin[0], g0);
-        contract_eo<D, Q, +1>(tab + Tab::TB, tin[1], g1);
+        contract_pair<SR, D, Q, +1>(tab + Tab::TB, tin[0], tin[1], g0, g1);
         contract_eo<D, Q, -1>(tab + Tab::TG, tin[NC - 1], g2);
 #pragma unroll
         for (int c = 0; c < Q; ++c) {
@@ -355,13 +403,12 @@ struct DfmaEoBody {
             g2[c] = fma(d22, a2, fma(d12, a1, d02 * a0));
           }
         }
-        double w[D];
-        contract_eo<Q, D, +1>(tab + Tab::TBT, g0, w);
+        double w[D], w1[D];
+        contract_pair<SR, Q, D, +1>(tab + Tab::TBT, g0, g1, w, w1);
 #pragma unroll
         for (int k = 0; k < D; ++k) sw[LW::at(e, 0, a, b, k)] = w[k];
-        contract_eo<Q, D, +1>(tab + Tab::TBT, g1, w);
 #pragma unroll
-        for (int k = 0; k < D; ++k) sw[LW::at(e, 1, a, b, k)] = w[k];
+        for (int k = 0; k < D; ++k) sw[LW::at(e, 1, a, b, k)] = w1[k];
         contract_eo<Q, D, -1>(tab + Tab::TGT, g2, w);
 #pragma unroll
         for (int k = 0; k < D; ++k) sw[LW::at(e, 2, a, b, k)] = w[k];
@@ -385,19 +432,22 @@ struct DfmaEoBody {
       double wv[Q], r0[D];
 #pragma unroll
       for (int b = 0; b < Q; ++b) wv[b] = sw[LW::at(e, 0, a, b, k)];
-      contract_eo<Q, D, +1>(tab + Tab::TBT, wv, r0);  // rG = B^T w0 (BP1: r = B^T w)
-#pragma unroll
-      for (int j = 0; j < D; ++j) sr[LR::at(e, 0, a, j, k)] = r0[j];
       if constexpr (NC == 3) {
-        double r1[D];
+        double wv2[Q], r1[D], r2[D];
+#pragma unroll
+        for (int b = 0; b < Q; ++b) wv2[b] = sw[LW::at(e, 2, a, b, k)];
+        contract_pair<SR, Q, D, +1>(tab + Tab::TBT, wv, wv2, r0, r2);  // rG = B^T w0, B^T w2
+#pragma unroll
+        for (int j = 0; j < D; ++j) sr[LR::at(e, 0, a, j, k)] = r0[j];
 #pragma unroll
         for (int b = 0; b < Q; ++b) wv[b] = sw[LW::at(e, 1, a, b, k)];
-        contract_eo<Q, D, -1>(tab + Tab::TGT, wv, r0);  // G^T w1
+        contract_eo<Q, D, -1>(tab + Tab::TGT, wv, r1);  // G^T w1
 #pragma unroll
-        for (int b = 0; b < Q; ++b) wv[b] = sw[LW::at(e, 2, a, b, k)];
-        contract_eo<Q, D, +1>(tab + Tab::TBT, wv, r1);  // B^T w2
+        for (int j = 0; j < D; ++j) sr[LR::at(e, 1, a, j, k)] = r1[j] + r2[j];
+      } else {
+        contract_eo<Q, D, +1>(tab + Tab::TBT, wv, r0);  // r = B^T w
 #pragma unroll
-        for (int j = 0; j < D; ++j) sr[LR::at(e, 1, a, j, k)] = r0[j] + r1[j];
+        for (int j = 0; j < D; ++j) sr[LR::at(e, 0, a, j, k)] = r0[j];
       }
     });
   }

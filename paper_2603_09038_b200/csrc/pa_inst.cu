@@ -84,8 +84,9 @@ KernelEntry entry(int variant, int cfg) {
   return k;
 }
 
-template <int D, int Q, int NC, int E, bool IP, bool PP>
-using TunedEo = DfmaEoBody<D, Q, NC, E, round32(E * Q * Q), EoLayTuned<D, Q, NC, E, round32(E * Q * Q), IP>, PP>;
+template <int D, int Q, int NC, int E, bool IP, bool PP, bool SR = true>
+using TunedEo =
+    DfmaEoBody<D, Q, NC, E, round32(E * Q * Q), EoLayTuned<D, Q, NC, E, round32(E * Q * Q), IP>, PP, SR>;
 
 // nine tuned even-odd geometries from cfg c0: (E2, E1) x (smem D, D via L2) x
 // (W over T1, W over T2), then E0 in place
@@ -150,6 +151,8 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, true, true>(FK_VARIANT_EO, 29));
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 30));
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 31));
+  // cfg 32: cfg 29 with separate table-row loads per component (SR off)
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 32));
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;
   using M1 = TunedEo<D, Q, NC, E1, false, true>;
