@@ -80,6 +80,15 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
+// Same to a shared-window address, without a memory clobber: the copy lands
+// asynchronously and is only ordered by cp_async_wait_all (which clobbers)
+// and the CTA barrier after it, so nothing needs the compiler to re-read
+// shared memory around every gather (the clobber forced the element base
+// id to be reloaded per copy).
+__device__ __forceinline__ void cp_async8_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src));
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }

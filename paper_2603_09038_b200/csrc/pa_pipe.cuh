@@ -227,16 +227,16 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   auto issue_x = [&](int b, int gslot, double* xdst) {
     const int e0 = b * E, ne = min(E, nel - e0);
     if constexpr (XPRE) {
+      const uint32_t xs = smem_u32(xdst);
 #pragma unroll
       for (int r = 0; r < NXT; ++r) {
         const int e = x_el[r] >> 16;
         if (e >= E) continue;  // past the batch's E * D^3 slots
-        double* dst = xdst + x_off[r];
         if (e < ne) {
           const int g = GM == 1 ? gs[gslot * E + e] + x_rel[r] : gs[gslot * E * G::GS + x_rel[r]];
-          cp_async8(dst, x + g);
+          cp_async8_s(xs + 8u * (uint32_t)x_off[r], x + g);
         } else {
-          *dst = 0.0;
+          xdst[x_off[r]] = 0.0;
         }
       }
     } else {
