@@ -13,3 +13,4 @@ timeout 600 python bench.py --variant mf --no-cpu-baseline 2>&1 | tail -1 > gpur
 timeout 1200 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --sweep gpurun_out/sweep_$tag.jsonl > /dev/null 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 30 --csv --log-file gpurun_out/launches_$tag.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 for f in bench bench_ref cg_weak cg_strong mixed mixed_mf bench_mf; do echo "$f: $(head -c 300 gpurun_out/${f}_$tag.json)"; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pa_pipe -s 3 -c 1 -o gpurun_out/ncu_$tag python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
