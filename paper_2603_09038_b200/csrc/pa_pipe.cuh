@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
         int e, l;
         XA::map(t, e, l);
         double* dst = xdst + XA::off(e, l);
-        if (e < ne) cp_async8(dst, x + gid_of(gslot, e, l));
+        if (e < ne) cp_async8_s(smem_u32(dst), x + gid_of(gslot, e, l));
         else *dst = 0.0;
       }
     }
