@@ -1,6 +1,8 @@
 """Small applies for compute-sanitizer (memcheck / racecheck / synccheck):
 every default geometry at p=1..8 (BP1, BP3, PA and MF, with Dirichlet bits),
-the acoustic-gravity FusedPA/FusedMF apply and fused normal at orders 2..8."""
+the precomputed-gather / closed-form-id geometries (eo25-32, mf8-9) with and
+without Dirichlet bits, the acoustic-gravity FusedPA/FusedMF apply and fused
+normal at orders 2..8."""
 import os
 import sys
 
@@ -20,6 +22,19 @@ for p in range(1, 9):
             y = op.apply(x)
             assert bool(torch.isfinite(y).all())
             op.close()
+for p in (1, 2, 4, 5, 8):
+    for kind in ("diffusion", "mass"):
+        for variant, cfgs in (("eo", range(25, 33)), ("mf", (8, 9))):
+            for cfg in cfgs:
+                for dirichlet in (False, True):
+                    os.environ["FK_CFG"] = str(cfg)
+                    op = PAOperator(build_mesh(3, 2, 2), p, kind=kind, dirichlet=dirichlet,
+                                    strategy="MF" if variant == "mf" else "PA")
+                    x = torch.randn(op.num_dofs, dtype=torch.float64, device="cuda")
+                    y = op.apply(x)
+                    assert bool(torch.isfinite(y).all())
+                    op.close()
+os.environ.pop("FK_CFG", None)
 for p in range(2, 9):
     for strategy in ("FusedPA", "FusedMF"):
         mop = MixedOperator(build_mesh(2, 2, 3), p, p - 1, p + 1, strategy=strategy)
