@@ -60,12 +60,14 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // (variant, cfg) per order, best of profiles/r01_sweep_v21_shared_rows.jsonl
 // (BP3; one box, every candidate geometry incl. the precomputed-gather cfgs
 // 25-31, shared table rows) and r01_sweep_v19_xp.jsonl (BP1); BP3 p=4 from
-// the repeated A/B r01_ab_p4_cfg29_32.log (cfg 32 = 29 without shared rows,
-// +1.5%); tools/auto_table.py.  Structured-id geometries (eo19-24, 29-32)
-// fall back to cfg 0 when the caller passes its own gather map
+// the repeated A/Bs r01_ab_p4_cfg29_32.log and r01_ab_p4_cfg32_35.log (cfg 35:
+// four elements per CTA, W over T2, no shared rows, closed-form ids, one X
+// buffer, precomputed gather: +6% over cfg 32 over 1000 applies);
+// tools/auto_table.py.  Structured-id geometries (eo19-24, 29-35) fall back
+// to cfg 0 when the caller passes its own gather map
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg3[9] = {0, 19, 2, 2, 32, 25, 14, 18, 23};
+const int kAutoCfg3[9] = {0, 19, 2, 2, 35, 25, 14, 18, 23};
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
 const int kAutoCfg1[9] = {0, 18, 31, 31, 30, 23, 30, 23, 29};
 

@@ -153,6 +153,11 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 31));
   // cfg 32: cfg 29 with separate table-row loads per component (SR off)
   out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 32));
+  // cfgs 33-35: more SR-off closed-form geometries (33: W over T1; 34: two X
+  // buffers; 35: E1 elements per CTA, the BP3 p=4 default)
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 33));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true, false>, true, false, false, 1, false, true>(FK_VARIANT_EO, 34));
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, true, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 35));
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;
   using M1 = TunedEo<D, Q, NC, E1, false, true>;
