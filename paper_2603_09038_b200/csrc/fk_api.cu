@@ -77,10 +77,11 @@ int auto_variant(int nc, int p, int q) {
   return nc == 3 ? kAutoVar3[p] : kAutoVar1[p];
 }
 
-// matrix-free geometry per order (best of profiles/r01_sweep_v14_mf.jsonl; BP1
-// p=2/3 from r01_sweep_v20_mf_xp.jsonl, +8%/+5%)
-const int kAutoCfgMF3[9] = {0, 7, 3, 5, 5, 5, 6, 5, 6};
-const int kAutoCfgMF1[9] = {0, 3, 9, 8, 4, 5, 4, 4, 4};
+// matrix-free geometry per order (best of profiles/r01_sweep_v24_mf10.jsonl, the
+// earlier r01_sweep_v14_mf / v20_mf_xp where the new geometries do not win;
+// BP3 p=4 mf10 +6% over mf5 in a repeated A/B, r01_ab_mf_p4_cfg5_10.log)
+const int kAutoCfgMF3[9] = {0, 8, 10, 10, 10, 10, 6, 5, 6};
+const int kAutoCfgMF1[9] = {0, 3, 9, 8, 10, 10, 10, 10, 4};
 int auto_cfg_mf(int nc, int p) {
   if (p < 1 || p > 8) return 0;
   return nc == 3 ? kAutoCfgMF3[p] : kAutoCfgMF1[p];

@@ -180,6 +180,8 @@ void add_all(std::vector<KernelEntry>& out) {
   // (profiles/r01_sweep_v20_mf_xp.jsonl)
   out.push_back(entry<D, Q, NC, M1s, true, false, true, 1, false, true>(FK_VARIANT_MF, 8));
   out.push_back(entry<D, Q, NC, M0is, true, false, true, 1, false, true>(FK_VARIANT_MF, 9));
+  // mf10: the BP3 p=4 PA default's body (cfg 35) without the PA stream
+  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, true, true, false>, true, false, true, 1, true, true>(FK_VARIANT_MF, 10));
 }
 
 }  // namespace
