@@ -67,7 +67,7 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // to cfg 0 when the caller passes its own gather map
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg3[9] = {0, 19, 2, 2, 35, 25, 14, 18, 23};
+const int kAutoCfg3[9] = {0, 19, 2, 35, 35, 25, 14, 18, 23};  // p=3..7 confirmed by r01_ab_orders_3567.log
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
 const int kAutoCfg1[9] = {0, 18, 31, 31, 30, 23, 30, 23, 29};
 
