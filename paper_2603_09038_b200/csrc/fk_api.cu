@@ -69,7 +69,7 @@ constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
 const int kAutoCfg3[9] = {0, 19, 2, 35, 35, 25, 14, 18, 23};  // p=3..7 confirmed by r01_ab_orders_3567.log
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg1[9] = {0, 18, 31, 31, 30, 23, 30, 23, 29};
+const int kAutoCfg1[9] = {0, 18, 31, 31, 30, 35, 30, 23, 29};  // p=3,5-7: r01_ab_orders_3567_bp1.log
 
 int auto_variant(int nc, int p, int q) {
   (void)q;

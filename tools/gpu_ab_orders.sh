@@ -3,7 +3,7 @@ for p in 5 6 7 3; do
   case $p in 3) n=71;; 5) n=43;; 6) n=36;; 7) n=31;; esac
   for i in 1 2; do
     for c in $1; do
-      v=$(FK_CFG=$c timeout 300 python bench.py --p $p --n $n --steps 200 --warmup 10 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],2), round(d['roofline']['frac'],3))")
+      v=$(FK_CFG=$c timeout 300 python bench.py --p $p --n $n --steps 200 --warmup 10 --no-cpu-baseline ${KIND:+--kind $KIND} 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],2), round(d['roofline']['frac'],3))")
       echo "p $p rep $i cfg $c: $v"
     done
   done
