@@ -67,9 +67,9 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // to cfg 0 when the caller passes its own gather map
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg3[9] = {0, 19, 2, 35, 35, 25, 14, 18, 23};  // p=3..7 confirmed by r01_ab_orders_3567.log
+const int kAutoCfg3[9] = {0, 19, 35, 35, 35, 25, 14, 18, 23};  // every p by 200-apply A/B: r01_ab_orders_*.log
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg1[9] = {0, 18, 31, 31, 30, 35, 30, 23, 29};  // p=3,5-7: r01_ab_orders_3567_bp1.log
+const int kAutoCfg1[9] = {0, 24, 31, 31, 30, 35, 30, 23, 30};  // every p by 200-apply A/B: r01_ab_orders_*.log
 
 int auto_variant(int nc, int p, int q) {
   (void)q;
