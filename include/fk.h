@@ -134,14 +134,51 @@ int fk_op_set_essential(fk_op* op, double* v_dev, double value);
 int fk_cg_solve(fk_op* op, const double* b_dev, double* x_dev, int iters, double rtol,
                 double* hist_host, int* iters_done);
 
+/* Allocate the CG workspace (5 vectors, reduction scratch, a history of
+ * iters+1) so that a following fk_cg_solve with at most `iters` iterations
+ * makes no device allocation — ranks sharing one GPU (loopback group) call
+ * it on every rank before the collective solve. */
+int fk_cg_prepare(fk_op* op, int iters);
+
 /* Device reductions used by multi-rank CG and by tests. */
 int fk_dot(fk_op* op, const double* a_dev, const double* b_dev, double* host_out);
 
-/* Multi-GPU: one communicator per rank over NCCL.  nccl_unique_id points to
- * the 128-byte ncclUniqueId produced by fk_comm_unique_id on rank 0 and
- * broadcast by the caller (e.g. torch.distributed). */
+/* Multi-GPU: one communicator per rank (z-slab decomposition).
+ * Replaces the MPI group exchange of the paper's P / P^T;
+ * the reference itself is single-process (P = identity).
+ *
+ * Two transports:
+ *  FK_TRANSPORT_P2P   peer memory over NVLink / NVSwitch: each rank owns a
+ *                     mailbox (halo planes + flag words); neighbours store their
+ *                     partial interface planes straight into it and release a
+ *                     monotone flag; CG scalars are reduced by every rank
+ *                     storing its partial into every peer's slot array and
+ *                     summing the slots in rank order (bitwise identical on all
+ *                     ranks).  Kernel-only, so it is captured in the CG graph.
+ *  FK_TRANSPORT_NCCL  grouped ncclSend/ncclRecv + ncclAllReduce.
+ * nccl_unique_id points to the 128-byte ncclUniqueId produced by
+ * fk_comm_unique_id on rank 0 and broadcast by the caller. */
+#define FK_TRANSPORT_NCCL 1
+#define FK_TRANSPORT_P2P 2
+#define FK_MAX_RANKS 16
+#define FK_IPC_HANDLE_BYTES 64
+
 int fk_comm_unique_id(void* out128);
 int fk_comm_create(fk_comm** out, const void* nccl_unique_id, int rank, int nranks, int device);
+/* P2P across processes (one per GPU): allocate this rank's mailbox for halo
+ * planes of up to plane_cap doubles and return its CUDA-IPC handle
+ * (FK_IPC_HANDLE_BYTES); the caller all-gathers the handles (rank order) and
+ * passes them to fk_comm_connect_p2p on every rank. */
+int fk_comm_create_p2p(fk_comm** out, int rank, int nranks, int device, int64_t plane_cap,
+                       void* ipc_handle_out);
+int fk_comm_connect_p2p(fk_comm* comm, const void* all_handles);
+/* P2P inside one process: nranks communicators at once (out[0..nranks-1]),
+ * rank r on devices[r] (all equal = a loopback group on one GPU; distinct
+ * devices get peer access enabled).  Each rank must be driven by its own
+ * host thread and stream: the exchange waits on the device for the peers. */
+int fk_comm_create_loopback(fk_comm** out, int nranks, const int* devices, int64_t plane_cap);
+/* transport, rank, nranks of a communicator */
+int fk_comm_query(const fk_comm* comm, int* transport, int* rank, int* nranks);
 int fk_comm_destroy(fk_comm* comm);
 
 /* Benchmark hook: time `reps` applies with CUDA events on the handle's

@@ -280,16 +280,24 @@ class Problem:
         p = z.copy()
         nom = float(r @ z)
         hist = [np.sqrt(nom)]
+        # MFEM CGSolver: converged when nom <= max(rtol^2 nom0, abs_tol^2)
+        # (abs_tol = 0), which includes an exactly zero residual; break on
+        # p.Ap == 0
         stop = rtol * rtol * nom
+        if nom <= stop:
+            return x, np.array(hist)
         for _ in range(iters):
             Ap = A(p)
-            alpha = nom / float(p @ Ap)
+            den = float(p @ Ap)
+            if den == 0.0:
+                break
+            alpha = nom / den
             x += alpha * p
             r -= alpha * Ap
             z = dinv * r
             betanom = float(r @ z)
             hist.append(np.sqrt(betanom))
-            if rtol > 0 and betanom <= stop:
+            if betanom <= stop:
                 break
             beta = betanom / nom
             p = z + beta * p

@@ -30,6 +30,12 @@ FK_VARIANT_DMMA = 2
 FK_VARIANT_EO = 3
 FK_VARIANT_MF = 4
 
+FK_TRANSPORT_NCCL = 1
+FK_TRANSPORT_P2P = 2
+FK_MAX_RANKS = 16
+FK_IPC_HANDLE_BYTES = 64
+TRANSPORTS = {"nccl": FK_TRANSPORT_NCCL, "p2p": FK_TRANSPORT_P2P}
+
 VARIANTS = {"auto": FK_VARIANT_AUTO, "dfma": FK_VARIANT_DFMA, "dmma": FK_VARIANT_DMMA,
             "eo": FK_VARIANT_EO, "mf": FK_VARIANT_MF}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
@@ -41,7 +47,9 @@ EXPORTS = (
     "fk_op_pa_data",
     "fk_op_apply", "fk_op_apply_host", "fk_op_apply_local", "fk_op_diagonal",
     "fk_op_set_essential",
-    "fk_cg_solve", "fk_dot", "fk_comm_unique_id", "fk_comm_create", "fk_comm_destroy",
+    "fk_cg_prepare", "fk_cg_solve", "fk_dot", "fk_comm_unique_id", "fk_comm_create",
+    "fk_comm_create_p2p", "fk_comm_connect_p2p", "fk_comm_create_loopback", "fk_comm_query",
+    "fk_comm_destroy",
     "fk_op_time_apply",
     "fk_mix_create", "fk_mix_setup", "fk_mix_destroy", "fk_mix_get_info", "fk_mix_apply",
     "fk_mix_fused_normal", "fk_mix_mass_inverse", "fk_mix_rk4", "fk_mix_lumped",
@@ -168,10 +176,15 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "fk_op_apply_local": (i, [vp, vp, vp]),
         "fk_op_diagonal": (i, [vp, vp]),
         "fk_op_set_essential": (i, [vp, vp, d]),
+        "fk_cg_prepare": (i, [vp, i]),
         "fk_cg_solve": (i, [vp, vp, vp, i, d, pd, ctypes.POINTER(i)]),
         "fk_dot": (i, [vp, vp, vp, pd]),
         "fk_comm_unique_id": (i, [vp]),
         "fk_comm_create": (i, [ctypes.POINTER(vp), vp, i, i, i]),
+        "fk_comm_create_p2p": (i, [ctypes.POINTER(vp), i, i, i, i64, vp]),
+        "fk_comm_connect_p2p": (i, [vp, vp]),
+        "fk_comm_create_loopback": (i, [ctypes.POINTER(vp), i, ctypes.POINTER(i), i64]),
+        "fk_comm_query": (i, [vp, ctypes.POINTER(i), ctypes.POINTER(i), ctypes.POINTER(i)]),
         "fk_comm_destroy": (i, [vp]),
         "fk_op_time_apply": (i, [vp, vp, vp, i, vp, ctypes.c_size_t, pd, pd]),
         "fk_mix_create": (i, [ctypes.POINTER(vp), ctypes.POINTER(FkMixDesc)]),

@@ -211,14 +211,23 @@ int launch_range(fk_op* op, const double* x, double* y, int64_t e0, int64_t ne, 
 }
 
 // Multi-rank apply with the interface exchange overlapped:
-// boundary element layers first, then the NCCL plane swap on the comm stream
-// runs while the interior layers (which never touch an interface plane)
-// compute; the received partial sums are added after the join.
+// boundary element layers first, then the plane exchange runs while the
+// interior layers (which never touch an interface plane) compute; the
+// received partial sums are added after the join.
 int apply_overlapped(fk_op* op, const double* x, double* y) {
   const int64_t nxy = (int64_t)op->desc.nx * op->desc.ny;
   FK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * op->ndof, op->stream));
   FK_TRY(launch_range(op, x, y, 0, nxy, op->stream));
   FK_TRY(launch_range(op, x, y, op->nel - nxy, nxy, op->stream));
+  if (fk::p2p(op)) {
+    // peer memory: the plane stores are issued in stream order before the
+    // interior kernel (a few µs of NVLink stores that never wait behind the
+    // persistent grid); the data lands in the neighbours' mailboxes while the
+    // interior layers run, and the add waits on the arrival flags after them
+    FK_TRY(fk::exchange_post(op, y, op->stream));
+    FK_TRY(launch_range(op, x, y, nxy, op->nel - 2 * nxy, op->stream));
+    return fk::exchange_finish(op, y, op->stream);
+  }
   FK_CUDA(cudaEventRecord(op->ev_bnd, op->stream));
   FK_CUDA(cudaStreamWaitEvent(op->comm_stream, op->ev_bnd, 0));
   FK_TRY(fk::exchange_post(op, y, op->comm_stream));
@@ -232,7 +241,7 @@ int apply_full(fk_op* op, const double* x, double* y, cudaStream_t s_override = 
   cudaStream_t saved = op->stream;
   if (s_override) op->stream = s_override;
   int rc = FK_OK;
-  if (op->comm && op->comm->nranks > 1 && op->desc.nz_local >= 3) {
+  if (fk::multi_rank(op) && op->desc.nz_local >= 3) {
     rc = apply_overlapped(op, x, y);
   } else {
     rc = launch_local(op, x, y);
@@ -249,6 +258,46 @@ int apply_full(fk_op* op, const double* x, double* y, cudaStream_t s_override = 
 }
 
 }  // namespace
+
+// With CUDA lazy module loading (the default since CUDA 12.2) the first launch
+// of a kernel may need a context synchronisation; if a peer rank's exchange
+// kernel is spinning on this device at that moment (a loopback group, or any
+// rank waiting for a neighbour), that synchronisation never completes.  So a
+// multi-rank operator loads, at setup, every kernel its apply / diagonal /
+// dot / CG paths can launch (cudaFuncGetAttributes forces the load).
+static int preload_kernels(const fk_op* op) {
+  const void* ks[] = {reinterpret_cast<const void*>(&fk::ess_copy_kernel),
+                      reinterpret_cast<const void*>(&fk::ess_set_kernel),
+                      reinterpret_cast<const void*>(&fk::dot_kernel),
+                      reinterpret_cast<const void*>(&fk::cg_init_kernel),
+                      reinterpret_cast<const void*>(&fk::cg_start_kernel),
+                      reinterpret_cast<const void*>(&fk::cg_alpha_kernel),
+                      reinterpret_cast<const void*>(&fk::cg_update_kernel),
+                      reinterpret_cast<const void*>(&fk::cg_finish_kernel),
+                      reinterpret_cast<const void*>(&fk::cg_dir_kernel),
+                      reinterpret_cast<const void*>(&fk::recip_kernel)};
+  cudaFuncAttributes a;
+  for (const void* k : ks) FK_CUDA(cudaFuncGetAttributes(&a, k));
+  for (const auto& k : registry()) {
+    if (k.nc != op->nc || k.d != op->d || k.q != op->q) continue;
+    FK_CUDA(cudaFuncGetAttributes(&a, k.func));
+    if (k.diag_func) FK_CUDA(cudaFuncGetAttributes(&a, k.diag_func));
+  }
+  return fk::preload_comm_kernels();
+}
+
+// reduction scratch (block partials, last-block counters, CG scalars); made at
+// setup so that dots and CG solves allocate nothing while peers may be waiting
+static int ensure_reduce_ws(fk_op* op) {
+  if (op->partials == nullptr) {
+    FK_CUDA(cudaMalloc(&op->partials, sizeof(double) * 4096));
+    FK_CUDA(cudaMalloc(&op->counter, sizeof(unsigned) * 4));
+    FK_CUDA(cudaMemsetAsync(op->counter, 0, sizeof(unsigned) * 4, op->stream));
+    FK_CUDA(cudaMalloc(&op->scal, sizeof(double) * 16 + sizeof(int) * 8));
+    FK_CUDA(cudaMemsetAsync(op->scal, 0, sizeof(double) * 16 + sizeof(int) * 8, op->stream));
+  }
+  return FK_OK;
+}
 
 int fk_set_error(int code, const char* msg) { return fail(code, "%s", msg); }
 
@@ -442,6 +491,9 @@ int fk_op_setup(fk_op* op) {
     FK_CUDA(cudaEventCreate(&op->ev3));
   }
   if (op->comm) FK_TRY(fk::comm_setup(op));
+  if (fk::multi_rank(op)) FK_TRY(preload_kernels(op));
+  FK_TRY(ensure_reduce_ws(op));
+  FK_CUDA(cudaStreamSynchronize(s));
   op->is_setup = true;
   return select_kernel(op, op->desc.variant);
 }
@@ -649,16 +701,6 @@ int fk_op_set_essential(fk_op* op, double* v, double value) {
   return FK_OK;
 }
 
-static int ensure_reduce_ws(fk_op* op) {
-  if (op->partials == nullptr) {
-    FK_CUDA(cudaMalloc(&op->partials, sizeof(double) * 4096));
-    FK_CUDA(cudaMalloc(&op->counter, sizeof(unsigned) * 4));
-    FK_CUDA(cudaMemset(op->counter, 0, sizeof(unsigned) * 4));
-    FK_CUDA(cudaMalloc(&op->scal, sizeof(double) * 16 + sizeof(int) * 8));
-    FK_CUDA(cudaMemset(op->scal, 0, sizeof(double) * 16 + sizeof(int) * 8));
-  }
-  return FK_OK;
-}
 
 static int red_blocks(const fk_op* op) { return std::min(op->num_sms * 4, 4096); }
 
@@ -703,6 +745,23 @@ static int cg_iteration(fk_op* op, double* x, cudaStream_t s) {
   return FK_OK;
 }
 
+int fk_cg_prepare(fk_op* op, int iters) {
+  if (op == nullptr) return fail(FK_EINVAL, "null handle");
+  if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
+  if (iters < 0) return fail(FK_EINVAL, "iters must be >= 0");
+  DeviceGuard g(op->device);
+  if (op->work == nullptr) FK_CUDA(cudaMalloc(&op->work, sizeof(double) * 5 * op->ndof));
+  FK_TRY(ensure_reduce_ws(op));
+  if (op->hist_cap < iters + 1) {
+    if (op->hist) FK_CUDA(cudaFree(op->hist));
+    op->hist = nullptr;
+    FK_CUDA(cudaMalloc(&op->hist, sizeof(double) * (iters + 1)));
+    op->hist_cap = iters + 1;
+  }
+  if (op->cg_stream == nullptr) FK_CUDA(cudaStreamCreateWithFlags(&op->cg_stream, cudaStreamNonBlocking));
+  return FK_OK;
+}
+
 int fk_cg_solve(fk_op* op, const double* b, double* x, int iters, double rtol, double* hist_host,
                 int* iters_done) {
   if (op == nullptr || b == nullptr || x == nullptr) return fail(FK_EINVAL, "null argument");
@@ -710,14 +769,7 @@ int fk_cg_solve(fk_op* op, const double* b, double* x, int iters, double rtol, d
   if (iters < 0) return fail(FK_EINVAL, "iters must be >= 0");
   DeviceGuard g(op->device);
   const int64_t n = op->ndof;
-  if (op->work == nullptr) FK_CUDA(cudaMalloc(&op->work, sizeof(double) * 5 * n));
-  FK_TRY(ensure_reduce_ws(op));
-  if (op->hist_cap < iters + 1) {
-    cudaFree(op->hist);
-    FK_CUDA(cudaMalloc(&op->hist, sizeof(double) * (iters + 1)));
-    op->hist_cap = iters + 1;
-  }
-  if (op->cg_stream == nullptr) FK_CUDA(cudaStreamCreateWithFlags(&op->cg_stream, cudaStreamNonBlocking));
+  FK_TRY(fk_cg_prepare(op, iters));
   cudaStream_t s = op->cg_stream;
   // order after the caller's stream
   FK_CUDA(cudaEventRecord(op->ev0, op->stream));
@@ -775,7 +827,11 @@ int fk_cg_solve(fk_op* op, const double* b, double* x, int iters, double rtol, d
   FK_CUDA(cudaMemcpyAsync(hi, iscal, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
   FK_CUDA(cudaStreamSynchronize(s));
   const int done_it = hi[fk::I_IT];
-  if (hist_host) FK_CUDA(cudaMemcpy(hist_host, op->hist, sizeof(double) * (done_it + 1), cudaMemcpyDeviceToHost));
+  if (hist_host) {
+    FK_CUDA(cudaMemcpyAsync(hist_host, op->hist, sizeof(double) * (done_it + 1),
+                            cudaMemcpyDeviceToHost, s));
+    FK_CUDA(cudaStreamSynchronize(s));
+  }
   if (iters_done) *iters_done = done_it;
   // make the caller's stream see the result
   FK_CUDA(cudaEventRecord(op->ev1, s));

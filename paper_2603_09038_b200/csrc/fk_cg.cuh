@@ -92,12 +92,19 @@ __global__ void cg_start_kernel(double* scal, int* iscal, double* hist, double r
   hist[0] = sqrt(nom);
   scal[S_STOP] = rtol * rtol * nom;
   iscal[I_IT] = 0;
-  iscal[I_DONE] = (rtol > 0.0 && nom <= 0.0) ? 1 : 0;
+  // MFEM CGSolver: converged when nom <= max(rtol^2 nom0, abs_tol^2), abs_tol
+  // = 0 — an exactly zero residual stops even with rtol = 0
+  iscal[I_DONE] = (nom <= rtol * rtol * nom) ? 1 : 0;
 }
 
-__global__ void cg_alpha_kernel(double* scal, const int* iscal) {
+__global__ void cg_alpha_kernel(double* scal, int* iscal) {
   if (iscal[I_DONE]) return;
-  scal[S_ALPHA] = scal[S_NOM] / scal[S_DEN];
+  const double den = scal[S_DEN];
+  if (den == 0.0) {  // MFEM breaks on p.Ap == 0 (no 0/0 update)
+    iscal[I_DONE] = 1;
+    return;
+  }
+  scal[S_ALPHA] = scal[S_NOM] / den;
 }
 
 // x += alpha p ; r -= alpha Ap ; z = dinv r ; partial r.z over [n0, n)
@@ -130,7 +137,7 @@ __global__ void cg_finish_kernel(double* scal, int* iscal, double* hist) {
   hist[it] = sqrt(bn);
   scal[S_BETA] = bn / scal[S_NOM];
   scal[S_NOM] = bn;
-  if (scal[S_STOP] > 0.0 && bn <= scal[S_STOP]) iscal[I_DONE] = 1;
+  if (bn <= scal[S_STOP]) iscal[I_DONE] = 1;
 }
 
 __global__ void cg_dir_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,

@@ -22,6 +22,7 @@ struct KernelEntry {
   bool structured = false;  // ids from the closed-form box restriction (no user gather map)
   size_t smem = 0;
   const void* func = nullptr;
+  const void* diag_func = nullptr;  // the assembled-diagonal kernel of this (d, q, nc)
   LaunchFn launch = nullptr;
   DiagFn diag = nullptr;
 };
@@ -61,9 +62,39 @@ const KernelEntry* find_kernel(int nc, int d, int q, int variant);
 
 }  // namespace fk
 
+namespace fk {
+constexpr int kMaxRanks = 16;
+
+// Per-rank mailbox of the peer-memory transport (fk_comm.cu), one device
+// allocation: control words, then the two halo planes.  Neighbours write into
+// it over NVLink (P2P stores through UVA or CUDA-IPC mappings); all flags are
+// monotone counters of completed exchanges / reductions, so the protocol
+// replays inside CUDA graphs without host involvement.
+struct Mailbox {
+  unsigned long long recv_flag[2];        // [0] plane from the rank below arrived, [1] from above
+  unsigned long long consumed[2];         // [0] the rank below has consumed my plane, [1] above
+  unsigned long long red_flag[kMaxRanks]; // reduction contribution of rank j arrived
+  unsigned long long seq_x, seq_r;        // completed exchanges / reductions (owner only)
+  unsigned int put_done, add_done;        // last-CTA counters of the put / add kernels
+  unsigned int pad[2];
+  double red_slot[2][kMaxRanks];          // contributions, double-buffered by parity
+};
+constexpr size_t kMailboxHeader = (sizeof(Mailbox) + 255) / 256 * 256;
+
+struct PeerTable {
+  Mailbox* box[kMaxRanks];  // every rank's mailbox as addressable from this rank
+};
+}  // namespace fk
+
 struct fk_comm {
+  int transport = FK_TRANSPORT_NCCL;
   void* nccl = nullptr;  // ncclComm_t
   int rank = 0, nranks = 1, device = 0;
+  // peer-memory transport
+  fk::Mailbox* box = nullptr;  // own mailbox (device)
+  fk::PeerTable peers{};
+  int64_t plane_cap = 0;       // doubles per halo plane
+  bool ipc_mapped[fk::kMaxRanks] = {};
 };
 
 struct fk_op {

@@ -81,6 +81,7 @@ KernelEntry entry(int variant, int cfg) {
   k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>);
   k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>;
   k.diag = &launch_diag<D, Q, NC>;
+  k.diag_func = reinterpret_cast<const void*>(&diagonal_kernel<D, Q, NC>);
   return k;
 }
 

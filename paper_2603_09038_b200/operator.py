@@ -183,6 +183,8 @@ class PAOperator:
         desc.variant = _lib.VARIANTS[variant]
         desc.device = self.device.index
         desc.stream = ctypes.c_void_p(self._stream.cuda_stream)
+        if comm is not None:
+            comm.attach((mesh.nx * self.order + 1) * (mesh.ny * self.order + 1))
         desc.comm = comm.handle if comm is not None else None
         self._lib = lib
         h = ctypes.c_void_p()
@@ -225,7 +227,7 @@ class PAOperator:
 
     @property
     def variant(self) -> str:
-        return _lib.VARIANT_NAMES[self._info().variant]
+        return _lib.VARIANT_NAMES[self.info.variant]
 
     def set_variant(self, variant: str) -> None:
         if variant not in _lib.VARIANTS:
@@ -267,10 +269,32 @@ class PAOperator:
             raise ValueError(f"{name} must be a contiguous float64 tensor on {self.device}")
         return v
 
+    def _host(self, v, name="vector"):
+        """A host buffer the C side may read/write num_dofs doubles through:
+        C-contiguous float64 NumPy array or CPU torch tensor of exactly that
+        length (anything else would overrun or corrupt memory)."""
+        torch = _torch()
+        if isinstance(v, torch.Tensor):
+            if v.is_cuda or v.dtype != torch.float64 or not v.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float64 CPU tensor")
+            self._check_vec(v, name)
+            return v.data_ptr()
+        if not isinstance(v, np.ndarray):
+            raise TypeError(f"{name} must be a NumPy array or a CPU torch tensor")
+        if v.dtype != np.float64 or not v.flags.c_contiguous:
+            raise ValueError(f"{name} must be a C-contiguous float64 array")
+        self._check_vec(v, name)
+        return v.ctypes.data
+
     def _count(self, n: int = 1) -> None:
+        """Reference counter semantics (counters.py:8-29, operator.py:280-286):
+        every apply bumps operator_applies and the flops; only the PA
+        strategies read stored quadrature data, the matrix-free ones count
+        no d_reads."""
         self.counters.operator_applies += n
         self.counters.flops += n * self.flops_per_apply
-        self.counters.d_reads += n * self._ncomp * self.num_quad_1d ** 3 * self.num_elements
+        if self.variant != "mf":
+            self.counters.d_reads += n * self._ncomp * self.num_quad_1d ** 3 * self.num_elements
 
     # -- apply ----------------------------------------------------------------
 
@@ -281,8 +305,9 @@ class PAOperator:
             xh = np.ascontiguousarray(x, dtype=np.float64)
             self._check_vec(xh, "state")
             yh = np.empty_like(xh) if out is None else out
+            yp = self._host(yh, "out")
             self._count()
-            _lib.check(self._lib.fk_op_apply_host(self._h, xh.ctypes.data, yh.ctypes.data))
+            _lib.check(self._lib.fk_op_apply_host(self._h, xh.ctypes.data, yp))
             return yh
         x = self._dev(x, "state")
         y = torch.empty_like(x) if out is None else self._dev(out, "out")
@@ -297,11 +322,9 @@ class PAOperator:
 
     def apply_host(self, x: np.ndarray, out: np.ndarray) -> np.ndarray:
         """Host-buffer apply without allocation (pinned ``x``/``out`` give full PCIe speed)."""
+        xp, yp = self._host(x, "x"), self._host(out, "out")
         self._count()
-        _lib.check(self._lib.fk_op_apply_host(self._h, x.ctypes.data if isinstance(x, np.ndarray)
-                                              else x.data_ptr(),
-                                              out.ctypes.data if isinstance(out, np.ndarray)
-                                              else out.data_ptr()))
+        _lib.check(self._lib.fk_op_apply_host(self._h, xp, yp))
         return out
 
     def apply_local(self, x, out=None):
@@ -313,8 +336,8 @@ class PAOperator:
         _lib.check(self._lib.fk_op_apply_local(self._h, x.data_ptr(), y.data_ptr()))
         return y
 
-    def diagonal(self):
-        d = self.zeros()
+    def diagonal(self, out=None):
+        d = self.zeros() if out is None else self._dev(out, "out")
         _lib.check(self._lib.fk_op_diagonal(self._h, d.data_ptr()))
         return d
 
@@ -323,6 +346,10 @@ class PAOperator:
         self._dev(v, "v")
         _lib.check(self._lib.fk_op_set_essential(self._h, v.data_ptr(), float(value)))
         return v
+
+    def prepare_cg(self, iters: int) -> None:
+        """Allocate the CG workspace now (fk_cg_prepare)."""
+        _lib.check(self._lib.fk_cg_prepare(self._h, int(iters)))
 
     def dot(self, a, b) -> float:
         """Global (all-rank) dot product over owned dofs."""
@@ -366,24 +393,31 @@ class PAOperator:
 # ---------------------------------------------------------------------------
 
 
-def cg_solve(op: PAOperator, b, iters: int = 100, rtol: float = 0.0):
+def cg_solve(op: PAOperator, b, iters: int = 100, rtol: float = 0.0, out=None, barrier=None):
     """Jacobi-PCG on ``op`` (build it with dirichlet=True for BP3), x0 = 0.
 
     Returns (x, history) with history[k] = sqrt(r_k . z_k), k = 0..iters_done.
-    ``b`` may be a NumPy array (x returned as NumPy) or a CUDA tensor.
+    ``b`` may be a NumPy array (x returned as NumPy) or a CUDA tensor; ``out``
+    an optional preallocated CUDA solution vector.  ``barrier`` (callable) is
+    run after the workspace is allocated and before the solve starts — ranks
+    of a loopback group on one GPU pass a shared barrier so that no rank
+    allocates device memory while a peer waits on the device.
     """
     torch = _torch()
     host = isinstance(b, np.ndarray)
     bd = torch.as_tensor(np.ascontiguousarray(b, dtype=np.float64), device=op.device) if host else op._dev(b, "b")
     if host:
         op._check_vec(bd, "b")
-    x = torch.empty_like(bd)
+    x = torch.empty_like(bd) if out is None else op._dev(out, "x")
     hist = np.zeros(iters + 1)
     done = ctypes.c_int()
-    op._count(iters)
+    _lib.check(op._lib.fk_cg_prepare(op._h, int(iters)))
+    if barrier is not None:
+        barrier()
     _lib.check(op._lib.fk_cg_solve(op._h, bd.data_ptr(), x.data_ptr(), int(iters), float(rtol),
                                    hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                    ctypes.byref(done)))
+    op._count(done.value)  # applies actually run (rtol may stop early)
     hist = hist[: done.value + 1]
     return (x.cpu().numpy() if host else x), hist
 
@@ -394,27 +428,99 @@ def cg_solve(op: PAOperator, b, iters: int = 100, rtol: float = 0.0):
 
 
 class Comm:
-    """One NCCL communicator per rank for the z-slab exchange and CG dots.
+    """One z-slab communicator per rank.
 
-    The 128-byte ncclUniqueId is produced by rank 0 and broadcast over an
-    existing torch.distributed process group (any backend)."""
+    ``transport="p2p"`` (default): the peer-memory transport of fk_comm.cu —
+    each rank's mailbox is mapped into its peers with CUDA IPC (handles
+    all-gathered over ``group``, any torch.distributed backend), halo planes
+    and CG scalars move by NVLink stores with device-side flags.  The mailbox
+    is sized for interface planes of ``plane_cap`` doubles; with
+    ``plane_cap=None`` it is created by the first operator attached (every
+    rank attaches collectively, as it constructs its operator).
+    ``transport="nccl"``: grouped ncclSend/ncclRecv + ncclAllReduce; the
+    128-byte ncclUniqueId is produced by rank 0 and broadcast over ``group``.
 
-    def __init__(self, rank: int, world_size: int, device: int, group=None):
-        import torch.distributed as dist
+    ``Comm.loopback(n, plane_cap)`` builds n ranks inside this process (one
+    GPU or several); drive each rank from its own thread and stream
+    (``parallel.run_ranks``)."""
 
-        lib = _lib.load()
+    def __init__(self, rank: int, world_size: int, device: int, group=None,
+                 transport: str = "p2p", plane_cap: int | None = None):
+        if transport not in _lib.TRANSPORTS:
+            raise ValueError(f"transport must be one of {tuple(_lib.TRANSPORTS)}, got {transport!r}")
+        if not 0 <= rank < world_size:
+            raise ValueError(f"bad rank {rank} of {world_size}")
+        self._lib = _lib.load()
         self.rank, self.world_size, self.device = rank, world_size, device
-        uid = (ctypes.c_char * 128)()
-        if rank == 0:
-            _lib.check(lib.fk_comm_unique_id(uid))
-        payload = [bytes(uid)]
-        if world_size > 1:
-            dist.broadcast_object_list(payload, src=0, group=group)
-        uid = (ctypes.c_char * 128).from_buffer_copy(payload[0])
+        self.transport = transport
+        self.group = group
+        self.handle = None
+        self.plane_cap = None
+        if transport == "nccl":
+            import torch.distributed as dist
+
+            uid = (ctypes.c_char * 128)()
+            if rank == 0:
+                _lib.check(self._lib.fk_comm_unique_id(uid))
+            payload = [bytes(uid)]
+            if world_size > 1:
+                dist.broadcast_object_list(payload, src=0, group=group)
+            uid = (ctypes.c_char * 128).from_buffer_copy(payload[0])
+            h = ctypes.c_void_p()
+            _lib.check(self._lib.fk_comm_create(ctypes.byref(h), uid, rank, world_size, device))
+            self.handle = h
+        elif plane_cap is not None:
+            self._create_p2p(int(plane_cap))
+
+    def _create_p2p(self, plane_cap: int) -> None:
         h = ctypes.c_void_p()
-        _lib.check(lib.fk_comm_create(ctypes.byref(h), uid, rank, world_size, device))
-        self.handle = h
-        self._lib = lib
+        mine = (ctypes.c_char * _lib.FK_IPC_HANDLE_BYTES)()
+        _lib.check(self._lib.fk_comm_create_p2p(ctypes.byref(h), self.rank, self.world_size,
+                                                self.device, int(plane_cap), mine))
+        self.handle, self.plane_cap = h, int(plane_cap)
+        if self.world_size > 1:
+            import torch.distributed as dist
+
+            handles = [None] * self.world_size
+            dist.all_gather_object(handles, bytes(mine), group=self.group)
+            blob = (ctypes.c_char * (_lib.FK_IPC_HANDLE_BYTES * self.world_size)).from_buffer_copy(
+                b"".join(handles))
+            _lib.check(self._lib.fk_comm_connect_p2p(self.handle, blob))
+            # every rank's mappings exist before any rank stores into a peer
+            dist.barrier(group=self.group)
+
+    @classmethod
+    def loopback(cls, nranks: int, plane_cap: int, devices=None) -> list["Comm"]:
+        """``nranks`` P2P communicators in this process (rank r on devices[r],
+        default all on the current device)."""
+        lib = _lib.load()
+        if devices is None:
+            import torch
+
+            devices = [torch.cuda.current_device()] * nranks
+        if len(devices) != nranks:
+            raise ValueError(f"{len(devices)} devices do not match {nranks} ranks")
+        hs = (ctypes.c_void_p * nranks)()
+        devs = (ctypes.c_int * nranks)(*[int(d) for d in devices])
+        _lib.check(lib.fk_comm_create_loopback(hs, nranks, devs, int(plane_cap)))
+        out = []
+        for r in range(nranks):
+            c = cls.__new__(cls)
+            c._lib, c.rank, c.world_size, c.device = lib, r, nranks, int(devices[r])
+            c.transport, c.group, c.plane_cap = "p2p", None, int(plane_cap)
+            c.handle = ctypes.c_void_p(hs[r])
+            out.append(c)
+        return out
+
+    def attach(self, plane: int) -> None:
+        """Called by an operator with interface planes of ``plane`` dofs."""
+        if self.transport != "p2p":
+            return
+        if self.handle is None:
+            self._create_p2p(plane)
+        elif plane > self.plane_cap:
+            raise ValueError(f"interface plane of {plane} dofs does not match the communicator's "
+                             f"capacity ({self.plane_cap})")
 
     def slab(self, nz: int) -> tuple[int, int]:
         from .parallel import slab_range
@@ -424,4 +530,4 @@ class Comm:
     def close(self):
         if self.handle is not None and self.handle.value:
             self._lib.fk_comm_destroy(self.handle)
-            self.handle = None
+        self.handle = None

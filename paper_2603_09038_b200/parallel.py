@@ -7,10 +7,12 @@ z-slowest, mesh.py:100) and therefore the contiguous global dof slice
 [z0*p*npx*npy, (z1*p+1)*npx*npy) (dofs are z-slowest, mesh.py:164);
 neighbouring slices overlap in exactly one npx*npy plane.
 
-On the GPU the exchange is NCCL inside libfk_b200 (fk_comm.cu); the
-functions here are the same algorithm on host tensors over any
-torch.distributed group, used by the gloo tests to pin the partition math
-(tests/test_parallel.py) and by bench.py for rank bookkeeping.
+On the GPU the exchange lives inside libfk_b200 (fk_comm.cu: peer-memory
+mailboxes over NVLink, or NCCL); the functions here are the same algorithm
+on host tensors over any torch.distributed group, used by the gloo tests to
+pin the partition math (tests/test_parallel.py) and by bench.py for rank
+bookkeeping.  ``run_ranks`` drives an in-process (loopback) group: one host
+thread and one CUDA stream per rank.
 """
 
 from __future__ import annotations
@@ -88,3 +90,44 @@ def gather_global(y_local: np.ndarray, ndof_global: int, nx, ny, p, z0, z1, rank
     full[s:e] = torch.as_tensor(np.asarray(y_local)[s - ls:e - ls])
     dist.all_reduce(full, group=group)
     return full.numpy()
+
+
+def run_ranks(fn, nranks: int, streams=None, device=None):
+    """Run ``fn(rank, stream, barrier)`` for every rank of an in-process group
+    on its own thread with its own CUDA stream current (the P2P exchange
+    waits on the device for the peers, so ranks must be issued
+    concurrently; allocate device memory before, not inside, ``fn`` — a
+    device allocation may wait for a peer that is waiting for this rank).
+    Returns the list of results in rank order; re-raises the first
+    exception."""
+    import threading
+
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    if streams is None:
+        streams = [torch.cuda.Stream(device=dev) for _ in range(nranks)]
+    bar = threading.Barrier(nranks)
+    out, err = [None] * nranks, [None] * nranks
+
+    def body(r):
+        try:
+            with torch.cuda.device(dev), torch.cuda.stream(streams[r]):
+                out[r] = fn(r, streams[r], bar.wait)
+                streams[r].synchronize()
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err[r] = e
+            bar.abort()
+
+    ts = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in err:
+        if e is not None and not isinstance(e, threading.BrokenBarrierError):
+            raise e
+    for e in err:
+        if e is not None:
+            raise e
+    return out
