@@ -90,6 +90,7 @@ typedef struct fk_op_info {
   int elems_per_block; /* launch geometry of the fused kernel */
   int threads_per_block;
   int blocks;          /* persistent grid size */
+  int cfg;             /* compiled launch geometry index of that variant (fk_op_set_config) */
 } fk_op_info;
 
 int fk_version(void);

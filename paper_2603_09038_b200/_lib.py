@@ -92,6 +92,7 @@ class FkOpInfo(ctypes.Structure):
         ("elems_per_block", ctypes.c_int),
         ("threads_per_block", ctypes.c_int),
         ("blocks", ctypes.c_int),
+        ("cfg", ctypes.c_int),
     ]
 
 

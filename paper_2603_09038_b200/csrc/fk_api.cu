@@ -541,6 +541,7 @@ int fk_op_get_info(const fk_op* op, fk_op_info* info) {
   info->elems_per_block = op->kern ? op->kern->E : 0;
   info->threads_per_block = op->kern ? op->kern->T : 0;
   info->blocks = op->blocks;
+  info->cfg = op->kern ? op->kern->cfg : -1;
   return FK_OK;
 }
 
