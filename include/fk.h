@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FK_API_VERSION 1
+#define FK_API_VERSION 2
 
 #define FK_OK 0
 #define FK_EINVAL (-1)      /* invalid argument / shape ("... do not match ...") */
@@ -78,6 +78,12 @@ typedef struct fk_op_desc {
   int device;         /* CUDA ordinal */
   void* stream;       /* cudaStream_t (NULL: the legacy default stream) */
   fk_comm* comm;      /* NULL for one rank; else the z-slab communicator */
+  int deterministic;  /* 1: verification mode — elements in 8-colour order (colour =
+                         parities of ex, ey, ez; two elements of one colour share no
+                         node), one launch per colour in fixed order, so every dof sums
+                         its element contributions in the same order on every run:
+                         apply, diagonal and CG bitwise reproducible (the reference's
+                         sequential np.add.at is likewise order-fixed, mesh.py:133-137) */
 } fk_op_desc;
 
 typedef struct fk_op_info {

@@ -78,6 +78,7 @@ class FkOpDesc(ctypes.Structure):
         ("device", ctypes.c_int),
         ("stream", ctypes.c_void_p),
         ("comm", ctypes.c_void_p),
+        ("deterministic", ctypes.c_int),
     ]
 
 

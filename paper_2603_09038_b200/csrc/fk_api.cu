@@ -92,6 +92,23 @@ int auto_cfg(int nc, int p) {
   return nc == 3 ? kAutoCfg3[p] : kAutoCfg1[p];
 }
 
+// Fastest geometry that reads the gather-id array (no closed-form ids) per
+// order: the deterministic mode (colour-ordered rows) and user maps.  Best
+// array-map entries of profiles/r01_sweep_f6.jsonl.
+const int kArrayCfg3[9] = {0, 1, 1, 2, 1, 1, 1, 18, 11};
+const int kArrayCfg1[9] = {0, 28, 28, 28, 25, 25, 26, 15, 27};
+const int kArrayCfgMF3[9] = {0, 5, 7, 5, 5, 5, 6, 2, 2};
+const int kArrayCfgMF1[9] = {0, 3, 3, 3, 0, 5, 4, 4, 6};
+int array_cfg(int nc, int p, int variant) {
+  if (p < 1 || p > 8) return 0;
+  if (variant == FK_VARIANT_MF) return nc == 3 ? kArrayCfgMF3[p] : kArrayCfgMF1[p];
+  if (variant == FK_VARIANT_EO) return nc == 3 ? kArrayCfg3[p] : kArrayCfg1[p];
+  return 0;
+}
+
+// the kernel must read op->gids (user map, or colour-ordered rows)
+bool needs_array_map(const fk_op* op) { return !op->host_gids.empty() || op->colour; }
+
 fk::OpView view(const fk_op* op) {
   fk::OpView v;
   v.B = op->B;
@@ -114,17 +131,15 @@ fk::OpView view(const fk_op* op) {
 
 // Even-odd folding needs B[q-1-a][d-1-i] = B[a][i] and G[q-1-a][d-1-i] = -G[a][i]
 // (symmetric nodes and points, as Basis1D.nodal produces, tensor.py:101-119).
+// The folded kernels use one half of each mirror pair, i.e. the tables are
+// symmetrised.  Basis1D.nodal's monomial-coefficient tables are themselves
+// only symmetric to their rounding: up to 41 / 59 ulp of max|B| at p = 8
+// (q = 9 / 10; 2 ulp at p = 4), the same size as their deviation from exact
+// Lagrange values (7.5e-15 at p = 8).  The gate admits that
+// rounding (128 ulp of the table maximum) and nothing coarser, so the
+// symmetrisation moves no entry by more than 64 ulp of max|B|.
 bool tables_symmetric(const fk_op* op) {
-  const int d = op->d, q = op->q;
-  double mb = 0.0, mg = 0.0, eb = 0.0, eg = 0.0;
-  for (int a = 0; a < q; ++a)
-    for (int i = 0; i < d; ++i) {
-      mb = std::max(mb, std::fabs(op->B[a * d + i]));
-      mg = std::max(mg, std::fabs(op->G[a * d + i]));
-      eb = std::max(eb, std::fabs(op->B[a * d + i] - op->B[(q - 1 - a) * d + (d - 1 - i)]));
-      eg = std::max(eg, std::fabs(op->G[a * d + i] + op->G[(q - 1 - a) * d + (d - 1 - i)]));
-    }
-  return eb <= 1e-12 * mb && eg <= 1e-12 * mg;
+  return fk::mirror_symmetric(op->B, op->G, op->q, op->d);
 }
 
 int select_kernel(fk_op* op, int variant) {
@@ -139,11 +154,13 @@ int select_kernel(fk_op* op, int variant) {
   else if (variant == FK_VARIANT_AUTO) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, auto_cfg(op->nc, op->p));
   else if (variant == FK_VARIANT_MF) k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, auto_cfg_mf(op->nc, op->p));
   if (k == nullptr) k = fk::find_kernel(op->nc, op->d, op->q, v);
-  if (k != nullptr && k->structured && !op->host_gids.empty()) {
+  if (k != nullptr && k->structured && needs_array_map(op)) {
     if (op->cfg >= 0)
       return fail(FK_EUNSUPPORTED, "launch config %d uses the closed-form box restriction; "
-                                   "a user gather map was given", op->cfg);
-    k = fk::find_kernel(op->nc, op->d, op->q, v);  // cfg 0: array map
+                                   "%s", op->cfg, op->colour ? "the deterministic mode orders elements by colour"
+                                                             : "a user gather map was given");
+    k = fk::find_kernel_cfg(op->nc, op->d, op->q, v, array_cfg(op->nc, op->p, v));
+    if (k == nullptr || k->structured) k = fk::find_kernel(op->nc, op->d, op->q, v);  // cfg 0: array map
   }
   if (k == nullptr)
     return fail(FK_EUNSUPPORTED, "no %s kernel compiled for kind=%d p=%d q=%d",
@@ -157,18 +174,21 @@ int select_kernel(fk_op* op, int variant) {
       if (op->cfg >= 0)
         return fail(FK_EUNSUPPORTED, "launch config %d needs %zu B shared memory (> %d)", op->cfg,
                     k->smem, max_smem);
-      // default geometry too large: first compiled geometry that fits
+      // default geometry too large: first compiled geometry of this variant
+      // that fits (and reads the user's gather map if there is one)
       const fk::KernelEntry* alt = nullptr;
-      for (int c = 0; c < 32 && alt == nullptr; ++c) {
-        const fk::KernelEntry* t = fk::find_kernel_cfg(op->nc, op->d, op->q, v, c);
-        if (t && t->smem <= (size_t)max_smem) alt = t;
+      for (const auto& t : registry()) {
+        if (t.nc != op->nc || t.d != op->d || t.q != op->q || t.variant != v) continue;
+        if (t.structured && needs_array_map(op)) continue;
+        if (t.smem <= (size_t)max_smem) {
+          alt = &t;
+          break;
+        }
       }
       if (alt == nullptr) return fail(FK_EUNSUPPORTED, "no launch config fits in shared memory");
       k = alt;
     }
   }
-  op->kern = k;
-  op->variant = v;
   if (op->is_setup) {
     DeviceGuard g(op->device);
     FK_CUDA(cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -177,20 +197,37 @@ int select_kernel(fk_op* op, int variant) {
     FK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->func, k->T, k->smem));
     if (occ < 1) return fail(FK_EUNSUPPORTED, "fused kernel does not fit on an SM (smem %zu)", k->smem);
     const int64_t nbatch = (op->nel + k->E - 1) / k->E;
-    op->max_blocks = occ * op->num_sms;
-    if (op->block_cap > 0) op->max_blocks = std::min(op->max_blocks, op->block_cap);
+    int max_blocks = occ * op->num_sms;
+    if (op->block_cap > 0) max_blocks = std::min(max_blocks, op->block_cap);
+    op->max_blocks = max_blocks;
     op->blocks = k->persist
-                     ? (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)op->max_blocks))
+                     ? (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)max_blocks))
                      : (int)std::max<int64_t>(1, nbatch);
   }
+  // committed only now: a failed selection leaves the previous kernel in place
+  op->kern = k;
+  op->variant = v;
+  return FK_OK;
+}
+
+int launch_range(fk_op* op, const double* x, double* y, int64_t e0, int64_t ne, cudaStream_t s);
+
+// The fused kernel over every local element (y already zeroed): one launch,
+// or in the deterministic mode one launch per colour in colour order.
+int launch_all(fk_op* op, const double* x, double* y, cudaStream_t s) {
+  if (op->colour) {
+    for (int c = 0; c < 8; ++c)
+      FK_TRY(launch_range(op, x, y, op->colour_off[c], op->colour_off[c + 1] - op->colour_off[c], s));
+    return FK_OK;
+  }
+  op->kern->launch(view(op), x, y, op->blocks, s);
+  FK_CUDA(cudaGetLastError());
   return FK_OK;
 }
 
 int launch_local(fk_op* op, const double* x, double* y) {
   FK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * op->ndof, op->stream));
-  op->kern->launch(view(op), x, y, op->blocks, op->stream);
-  FK_CUDA(cudaGetLastError());
-  return FK_OK;
+  return launch_all(op, x, y, op->stream);
 }
 
 // Fused kernel over local elements [e0, e0 + ne) (gids / PA data offset views).
@@ -241,7 +278,7 @@ int apply_full(fk_op* op, const double* x, double* y, cudaStream_t s_override = 
   cudaStream_t saved = op->stream;
   if (s_override) op->stream = s_override;
   int rc = FK_OK;
-  if (fk::multi_rank(op) && op->desc.nz_local >= 3) {
+  if (fk::multi_rank(op) && op->desc.nz_local >= 3 && !op->colour) {
     rc = apply_overlapped(op, x, y);
   } else {
     rc = launch_local(op, x, y);
@@ -407,6 +444,14 @@ int fk_op_create(fk_op** out, const fk_op_desc* d) {
       op->host_gids[i] = (int)g;
     }
   }
+  op->colour = d->deterministic != 0;
+  if (op->colour && d->gather_ids != nullptr) {
+    delete op;
+    return fail(FK_EUNSUPPORTED, "the deterministic mode orders the box's elements by colour; "
+                                 "it does not take a user gather map");
+  }
+  for (int c = 0; c < 8; ++c)
+    op->colour_off[c + 1] = op->colour_off[c] + fk::colour_count(c, d->nx, d->ny, d->nz_local);
   op->device = d->device;
   op->stream = static_cast<cudaStream_t>(d->stream);
   op->comm = d->comm;
@@ -442,7 +487,8 @@ int fk_op_setup(fk_op* op) {
   if (op->gids == nullptr) FK_CUDA(cudaMalloc(&op->gids, sizeof(int) * (op->nel * op->gs + 16)));
   if (op->host_gids.empty()) {
     fk::restriction_kernel<<<grid_for(op->nel * op->gs, 256, op->num_sms), 256, 0, s>>>(
-        op->gids, op->desc.nx, op->desc.ny, op->desc.nz_local, op->p, op->npx, op->npy, op->gs);
+        op->gids, op->desc.nx, op->desc.ny, op->desc.nz_local, op->p, op->npx, op->npy, op->gs,
+        op->colour ? 1 : 0);
     FK_CUDA(cudaGetLastError());
   } else {
     std::vector<int> padded(op->nel * op->gs, 0);
@@ -545,13 +591,25 @@ int fk_op_get_info(const fk_op* op, fk_op_info* info) {
   return FK_OK;
 }
 
+// Switch variant / launch geometry; on failure the handle keeps the kernel,
+// variant and cfg it had (select_kernel commits only when it succeeds).
+static int reselect(fk_op* op, int variant, int cfg) {
+  const int old_cfg = op->cfg;
+  op->cfg = cfg;
+  int rc = select_kernel(op, variant);
+  if (rc != FK_OK) {
+    op->cfg = old_cfg;
+    return rc;
+  }
+  op->desc.variant = variant;
+  return FK_OK;
+}
+
 int fk_op_set_variant(fk_op* op, int variant) {
   if (op == nullptr) return fail(FK_EINVAL, "null handle");
   if (variant < FK_VARIANT_AUTO || variant > FK_VARIANT_LAST)
     return fail(FK_EINVAL, "unknown variant %d", variant);
-  op->desc.variant = variant;
-  op->cfg = -1;
-  return select_kernel(op, variant);
+  return reselect(op, variant, -1);
 }
 
 int fk_op_set_config(fk_op* op, int variant, int cfg) {
@@ -560,9 +618,7 @@ int fk_op_set_config(fk_op* op, int variant, int cfg) {
     return fail(FK_EINVAL, "bad variant %d / cfg %d", variant, cfg);
   if (fk::find_kernel_cfg(op->nc, op->d, op->q, variant, cfg) == nullptr)
     return fail(FK_EUNSUPPORTED, "no launch config %d for variant %d", cfg, variant);
-  op->cfg = cfg;
-  op->desc.variant = variant;
-  return select_kernel(op, variant);
+  return reselect(op, variant, cfg);
 }
 
 int fk_op_restriction(fk_op* op, int64_t* host_out) {
@@ -574,8 +630,11 @@ int fk_op_restriction(fk_op* op, int64_t* host_out) {
   FK_CUDA(cudaMemcpyAsync(tmp.data(), op->gids, sizeof(int) * tmp.size(), cudaMemcpyDeviceToHost,
                           op->stream));
   FK_CUDA(cudaStreamSynchronize(op->stream));
-  for (int64_t e = 0; e < op->nel; ++e)
-    for (int l = 0; l < d3; ++l) host_out[e * d3 + l] = (int64_t)tmp[e * op->gs + l] + op->dof_offset;
+  for (int64_t s = 0; s < op->nel; ++s) {
+    // rows are in the reference's element order except in the colour order
+    const int64_t e = op->colour ? fk::colour_element(s, op->desc.nx, op->desc.ny, op->desc.nz_local) : s;
+    for (int l = 0; l < d3; ++l) host_out[e * d3 + l] = (int64_t)tmp[s * op->gs + l] + op->dof_offset;
+  }
   return FK_OK;
 }
 
@@ -615,7 +674,7 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
     FK_CUDA(cudaMalloc(&op->stage_y, bytes));
   }
   const int nzl = op->desc.nz_local;
-  if (op->comm != nullptr || op->desc.dirichlet || nzl < 4 || op->kern == nullptr) {
+  if (op->comm != nullptr || op->desc.dirichlet || op->colour || nzl < 4 || op->kern == nullptr) {
     FK_CUDA(cudaMemcpyAsync(op->stage_x, xh, bytes, cudaMemcpyHostToDevice, op->stream));
     FK_TRY(apply_full(op, op->stage_x, op->stage_y));
     FK_CUDA(cudaMemcpyAsync(yh, op->stage_y, bytes, cudaMemcpyDeviceToHost, op->stream));
@@ -679,8 +738,19 @@ int fk_op_diagonal(fk_op* op, double* diag) {
   FK_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * op->ndof, op->stream));
   const fk::KernelEntry* k = fk::find_kernel(op->nc, op->d, op->q, FK_VARIANT_DFMA);
   if (k == nullptr || k->diag == nullptr) return fail(FK_EUNSUPPORTED, "no diagonal kernel");
-  k->diag(view(op), diag, op->nel, (int)std::min<int64_t>(op->nel, (int64_t)op->num_sms * 16),
-          op->stream);
+  if (op->colour) {
+    for (int c = 0; c < 8; ++c) {
+      const int64_t e0 = op->colour_off[c], ne = op->colour_off[c + 1] - e0;
+      if (ne == 0) continue;
+      fk::OpView v = view(op);
+      v.gids += e0 * op->gs;
+      v.pa += e0 * op->ps;
+      k->diag(v, diag, ne, (int)std::min<int64_t>(ne, (int64_t)op->num_sms * 16), op->stream);
+    }
+  } else {
+    k->diag(view(op), diag, op->nel, (int)std::min<int64_t>(op->nel, (int64_t)op->num_sms * 16),
+            op->stream);
+  }
   FK_CUDA(cudaGetLastError());
   if (op->comm) FK_TRY(fk::exchange_interface(op, diag, op->stream));
   if (op->desc.dirichlet && op->n_ess > 0) {
@@ -857,8 +927,7 @@ int fk_op_time_apply(fk_op* op, const double* x, double* y, int reps, const void
     FK_CUDA(cudaEventRecord(e[0], op->stream));
     FK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * op->ndof, op->stream));
     FK_CUDA(cudaEventRecord(e[1], op->stream));
-    op->kern->launch(view(op), x, y, op->blocks, op->stream);
-    FK_CUDA(cudaGetLastError());
+    FK_TRY(launch_all(op, x, y, op->stream));
     FK_CUDA(cudaEventRecord(e[2], op->stream));
     if (op->comm) rc = fk::exchange_interface(op, y, op->stream);
     if (op->desc.dirichlet && op->n_ess > 0)

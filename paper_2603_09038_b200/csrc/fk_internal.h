@@ -52,8 +52,52 @@ inline int64_t pa_stride(int npa, int q) {
   while (((n - q * q) % 16 + 16) % 16 > 1) n += 2;
   return n;
 }
+// Colour-major element order of the deterministic mode: colour c = cx + 2 cy
+// + 4 cz holds the elements with (ex, ey, ez) = (cx, cy, cz) mod 2, each
+// colour lexicographic (x fastest).  Slot s of colour c (t = s - off[c]):
+// ex = cx + 2 (t % nxc), ey = cy + 2 ((t / nxc) % nyc), ez = cz + 2 (t / (nxc nyc)),
+// nxc = (nx + 1 - cx) / 2 etc.
+__host__ __device__ inline int64_t colour_count(int c, int nx, int ny, int nz) {
+  return (int64_t)((nx + 1 - (c & 1)) / 2) * ((ny + 1 - ((c >> 1) & 1)) / 2) *
+         ((nz + 1 - (c >> 2)) / 2);
+}
+__host__ __device__ inline int64_t colour_element(int64_t s, int nx, int ny, int nz) {
+  int c = 0;
+  int64_t off = 0;
+  for (; c < 7; ++c) {
+    const int64_t n = colour_count(c, nx, ny, nz);
+    if (s < off + n) break;
+    off += n;
+  }
+  const int64_t t = s - off;
+  const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+  const int64_t nxc = (nx + 1 - cx) / 2, nyc = (ny + 1 - cy) / 2;
+  const int64_t ex = cx + 2 * (t % nxc), ey = cy + 2 * ((t / nxc) % nyc), ez = cz + 2 * (t / (nxc * nyc));
+  return ex + (int64_t)nx * (ey + (int64_t)ny * ez);
+}
+
 inline int64_t gid_stride(int d) { return ((int64_t)d * d * d + 3) / 4 * 4; }
 inline int64_t bits_stride(int d) { return (((int64_t)d * d * d + 31) / 32 + 3) / 4 * 4; }
+
+// Mirror symmetry of a 1D table pair, B[q-1-a][d-1-i] = B[a][i] and
+// G[q-1-a][d-1-i] = -G[a][i] (G may be null), to 128 ulp of the table
+// maximum — the rounding of Basis1D.nodal's own tables (fk_api.cu:
+// tables_symmetric); the even-odd folded kernels need it.
+inline bool mirror_symmetric(const double* B, const double* G, int q, int d) {
+  double mb = 0.0, mg = 0.0, eb = 0.0, eg = 0.0;
+  for (int a = 0; a < q; ++a)
+    for (int i = 0; i < d; ++i) {
+      const int j = (q - 1 - a) * d + (d - 1 - i);
+      mb = mb > __builtin_fabs(B[a * d + i]) ? mb : __builtin_fabs(B[a * d + i]);
+      eb = eb > __builtin_fabs(B[a * d + i] - B[j]) ? eb : __builtin_fabs(B[a * d + i] - B[j]);
+      if (G) {
+        mg = mg > __builtin_fabs(G[a * d + i]) ? mg : __builtin_fabs(G[a * d + i]);
+        eg = eg > __builtin_fabs(G[a * d + i] + G[j]) ? eg : __builtin_fabs(G[a * d + i] + G[j]);
+      }
+    }
+  const double tol = 128.0 * 2.220446049250313e-16;
+  return eb <= tol * mb && eg <= tol * mg;
+}
 
 const KernelEntry* find_kernel_cfg(int nc, int d, int q, int variant, int cfg);
 
@@ -105,6 +149,8 @@ struct fk_op {
   double B[100], G[100], w[10];
   double jinv[3];
   std::vector<int> host_gids;  // optional user map (local ids)
+  bool colour = false;         // deterministic mode: colour-major element order
+  int64_t colour_off[9] = {};  // element range [colour_off[c], colour_off[c+1]) of colour c
   cudaStream_t stream = nullptr;  // user stream
   cudaStream_t cg_stream = nullptr;
   int device = 0, num_sms = 0;

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "fk_error.h"
+#include "fk_internal.h"
 #include "mix_kernels.h"
 
 namespace {
@@ -241,6 +242,11 @@ int fk_mix_create(fk_mix** out, const fk_mix_desc* d) {
     return fk_fail(FK_EINVAL, "non-positive Jacobian determinant in element 0");
   if (d->Bp == nullptr || d->Gp == nullptr || d->Bu == nullptr || d->w == nullptr)
     return fk_fail(FK_EINVAL, "basis tables Bp, Gp, Bu, w are required");
+  // the fused kernel folds the 1D tables even-odd (mix_pipe.cuh)
+  if (!fk::mirror_symmetric(d->Bp, d->Gp, d->num_quad_1d, d->order_p + 1) ||
+      !fk::mirror_symmetric(d->Bu, nullptr, d->num_quad_1d, d->order_u + 1))
+    return fk_fail(FK_EUNSUPPORTED, "the block operator kernels need mirror-symmetric basis tables "
+                                    "(symmetric nodes and quadrature points)");
   fk_mix* m = new fk_mix();
   m->desc = *d;
   m->dp = d->order_p + 1;

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 
+#include "fk_internal.h"
 #include "pa_common.cuh"
 
 namespace fk {
@@ -14,18 +15,21 @@ namespace fk {
 // The slab-local id plus dof_offset = z0*p*npx*npy is the reference's global id.
 // Rows are padded to gs int32 (16-byte multiples for the bulk copies);
 // padding entries hold a valid id (0) and are never used.
+// colour = 1: row s holds element colour_element(s) (deterministic mode,
+// fk_internal.h).
 __global__ void restriction_kernel(int* __restrict__ gids, int nx, int ny, int nzl, int p,
-                                   int64_t npx, int64_t npy, int64_t gs) {
+                                   int64_t npx, int64_t npy, int64_t gs, int colour) {
   const int d = p + 1, d3 = d * d * d;
   const int64_t total = (int64_t)nx * ny * nzl * gs;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = t / gs;
-    const int l = (int)(t - e * gs);
+    const int64_t row = t / gs;
+    const int l = (int)(t - row * gs);
     if (l >= d3) {
       gids[t] = 0;
       continue;
     }
+    const int64_t e = colour ? colour_element(row, nx, ny, nzl) : row;
     const int i = l % d, j = (l / d) % d, k = l / (d * d);
     const int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / ((int64_t)nx * ny);
     gids[t] = (int)((ex * p + i) + npx * ((ey * p + j) + npy * (ez * p + k)));

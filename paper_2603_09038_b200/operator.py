@@ -105,7 +105,11 @@ class PAOperator:
     paper_2603_09038_b200.fem.Mesh); ``basis`` defaults to
     Basis1D.nodal(order+1, num_quad_1d) and may be the reference's Basis1D;
     ``restriction`` (optional) is a Restriction whose gather_ids the device
-    map is built from instead of the closed form.
+    map is built from instead of the closed form.  ``deterministic=True`` is
+    the verification mode: elements run in 8-colour order with one launch
+    per colour, so every dof sums its contributions in a fixed order and
+    apply / diagonal / cg_solve are bitwise reproducible run to run (the
+    reference's np.add.at scatter is sequential, mesh.py:133-137).
     """
 
     def __init__(self, mesh, order: int, num_quad_1d: int | None = None,
@@ -113,7 +117,7 @@ class PAOperator:
                  dirichlet: bool = False, counters: Counters | None = None,
                  device=None, basis=None, restriction=None, variant: str = "auto",
                  comm: "Comm | None" = None, z_range: tuple[int, int] | None = None,
-                 stream=None):
+                 stream=None, deterministic: bool = False):
         if kind not in KINDS:
             raise ValueError(f"kind must be one of {tuple(KINDS)}, got {kind!r}")
         if strategy not in STRATEGIES:
@@ -180,6 +184,10 @@ class PAOperator:
             self._gids_host = ids
             desc.gather_ids = ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
         desc.dirichlet = 1 if self.dirichlet else 0
+        # verification mode: colour-ordered elements, bitwise reproducible
+        # y, diagonal and CG (fk.h fk_op_desc.deterministic)
+        self.deterministic = bool(deterministic)
+        desc.deterministic = 1 if self.deterministic else 0
         desc.variant = _lib.VARIANTS[variant]
         desc.device = self.device.index
         desc.stream = ctypes.c_void_p(self._stream.cuda_stream)
@@ -440,9 +448,14 @@ class Comm:
     ``transport="nccl"``: grouped ncclSend/ncclRecv + ncclAllReduce; the
     128-byte ncclUniqueId is produced by rank 0 and broadcast over ``group``.
 
-    ``Comm.loopback(n, plane_cap)`` builds n ranks inside this process (one
-    GPU or several); drive each rank from its own thread and stream
-    (``parallel.run_ranks``)."""
+    ``Comm.loopback(n, plane_cap, devices)`` builds n ranks inside this
+    process, one per GPU; drive each rank from its own thread and stream
+    (``parallel.run_ranks``).  Ranks that share ONE GPU belong in separate
+    processes (CUDA-IPC path above): kernels of different streams of one
+    process are not guaranteed to run concurrently (streams may share a
+    hardware queue), so a rank waiting on the device for a peer in the same
+    process can stall; contexts of different processes are time-sliced with
+    preemption and always progress (tests/_rankpool.py)."""
 
     def __init__(self, rank: int, world_size: int, device: int, group=None,
                  transport: str = "p2p", plane_cap: int | None = None):

@@ -94,10 +94,12 @@ def gather_global(y_local: np.ndarray, ndof_global: int, nx, ny, p, z0, z1, rank
 
 def run_ranks(fn, nranks: int, streams=None, device=None):
     """Run ``fn(rank, stream, barrier)`` for every rank of an in-process group
-    on its own thread with its own CUDA stream current (the P2P exchange
-    waits on the device for the peers, so ranks must be issued
-    concurrently; allocate device memory before, not inside, ``fn`` — a
-    device allocation may wait for a peer that is waiting for this rank).
+    (``Comm.loopback``, one GPU per rank) on its own thread with its own CUDA
+    stream current (the P2P exchange waits on the device for the peers, so
+    ranks must be issued concurrently; allocate device memory before, not
+    inside, ``fn`` — a device allocation may wait for a peer that is
+    waiting for this rank).  Ranks sharing one GPU should be processes, not
+    threads (see ``Comm``).
     Returns the list of results in rank order; re-raises the first
     exception."""
     import threading

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version():
-    assert _lib.load().fk_version() == 1
+    assert _lib.load().fk_version() == 2
 
 
 def _desc(**kw):

@@ -1,38 +1,27 @@
 """The multi-rank library path (z-slabs) executed for real.
 
-Every test builds a group of nranks = 2..4 z-slab operators on ONE GPU and
-drives each rank from its own host thread and CUDA stream through the C-ABI:
-
-* in-process (loopback) groups: ``Comm.loopback`` — the peer-memory
-  transport of fk_comm.cu with every rank's mailbox on this device, i.e. the
-  same put / flag / add kernels and slot allreduce that run over NVLink on
-  an 8-GPU box, including apply_overlapped (nz_local >= 3), the owned-dof
-  dots, slab Dirichlet faces and the CUDA-graph-captured CG;
-* two processes: ``Comm(transport="p2p")`` with the mailboxes mapped through
-  CUDA IPC, bootstrapped over gloo — the path bench.py --gpus N takes.
-
-Results are compared with the single-process CPU oracle on the same global
-mesh (normwise 1e-12; CG: identical iteration counts, histories within
-1e-8 h_0, as tests/test_gpu_parity.py) and shared planes must be
+Groups of nranks = 2..4 rank PROCESSES (tests/_rankpool.py) share cuda:0,
+each with its own CUDA context, exactly as one process per GPU on an 8-GPU
+box: the peer-memory transport of fk_comm.cu with the mailboxes mapped
+through CUDA IPC (bootstrap over gloo), the put / flag / add kernels, the
+rank-ordered slot allreduce, apply_overlapped (nz_local >= 3), the owned-dof
+dots, slab Dirichlet faces, the diagonal exchange and the CUDA-graph-captured
+CG.  Results are compared with the single-process CPU oracle on the same
+global mesh (normwise 1e-12; CG: identical iteration counts, histories within
+1e-8 h_0, as tests/test_gpu_parity.py), and shared interface planes must be
 bit-identical on both neighbours.
 """
-
-import os
-import subprocess
-import sys
 
 import numpy as np
 import pytest
 
 from _util import PARITY_TOL, normwise
 from oracle import bp
-from paper_2603_09038_b200 import Comm, PAOperator, cg_solve, fem, parallel
+from paper_2603_09038_b200 import Comm, PAOperator, fem, parallel
 
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
-
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -41,57 +30,32 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
-def dev(x):
-    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device="cuda")
+_POOLS = {}
 
 
-class Group:
-    """nranks z-slab operators of one global mesh on a loopback group."""
+@pytest.fixture(scope="module")
+def pools():
+    from _rankpool import RankPool
 
-    def __init__(self, kind, n, p, world, dirichlet=False, variant="auto", q=None):
-        self.kind, self.n, self.p, self.world = kind, n, p, world
-        nx, ny, nz = n
-        self.plane = parallel.plane_size(nx, ny, p)
-        self.comms = Comm.loopback(world, self.plane)
-        self.streams = [torch.cuda.Stream() for _ in range(world)]
-        mesh = fem.build_mesh(*n)
-        self.ops, self.ranges = [], []
-        for r in range(world):
-            self.ops.append(PAOperator(mesh, p, q, kind=kind, dirichlet=dirichlet, comm=self.comms[r],
-                                       stream=self.streams[r], variant=variant))
-            z0, z1 = self.comms[r].slab(nz)
-            self.ranges.append(parallel.local_dof_range(nx, ny, p, z0, z1))
-        self.P = bp.Problem(kind, *n, p, q)
+    def get(world):
+        if world not in _POOLS:
+            _POOLS[world] = RankPool(world)
+        return _POOLS[world]
 
-    def local(self, x):
-        return [dev(x[s:e]) for s, e in self.ranges]
+    yield get
+    for p in _POOLS.values():
+        p.close()
+    _POOLS.clear()
 
-    def empty(self):
-        return [torch.empty(e - s, dtype=torch.float64, device="cuda") for s, e in self.ranges]
 
-    def run(self, fn):
-        torch.cuda.synchronize()
-        return parallel.run_ranks(fn, self.world, streams=self.streams)
-
-    def assemble(self, parts):
-        """Global vector from the owned parts; checks both copies of every
-        shared plane are bitwise identical."""
-        y = np.zeros(self.P.ndof)
-        for r, ((s, e), v) in enumerate(zip(self.ranges, parts)):
-            v = v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v)
-            if r > 0:
-                prev = parts[r - 1]
-                prev = prev.cpu().numpy() if hasattr(prev, "cpu") else np.asarray(prev)
-                assert np.array_equal(prev[-self.plane:], v[:self.plane]), \
-                    f"shared plane of ranks {r - 1}/{r} differs"
-            y[s:e] = v
-        return y
-
-    def close(self):
-        for op in self.ops:
-            op.close()
-        for c in self.comms:
-            c.close()
+def assemble(parts, ndof, plane, key):
+    y = np.zeros(ndof)
+    for r, part in enumerate(parts):
+        if r > 0:
+            assert np.array_equal(parts[r - 1][key][-plane:], part[key][:plane]), \
+                f"shared plane of ranks {r - 1}/{r} differs"
+        y[part["lo"]:part["hi"]] = part[key]
+    return y
 
 
 CASES = [
@@ -107,49 +71,36 @@ CASES = [
 
 @pytest.mark.parametrize("kind,n,p,world", CASES)
 @pytest.mark.parametrize("dirichlet", [False, True])
-def test_loopback_apply_matches_oracle(kind, n, p, world, dirichlet):
-    g = Group(kind, n, p, world, dirichlet)
-    x = np.random.default_rng(7).standard_normal(g.P.ndof)
-    ess = g.P.boundary()
-    if dirichlet:
-        x[ess] = 0.0
-    ref = g.P.constrained_apply(x, ess) if dirichlet else g.P.apply(x)
-    xs, ys = g.local(x), g.empty()
-
-    def fn(r, s, bar):
-        for _ in range(3):  # repeated exchanges: the flag sequence advances
-            g.ops[r].apply(xs[r], out=ys[r])
-
-    g.run(fn)
-    y = g.assemble(ys)
+def test_multirank_apply_matches_oracle(pools, kind, n, p, world, dirichlet):
+    res = pools(world).run("apply", kind=kind, n=n, p=p, dirichlet=dirichlet)
+    P = bp.Problem(kind, *n, p)
+    x = np.random.default_rng(7).standard_normal(P.ndof)
+    ref = P.constrained_apply(x, P.boundary()) if dirichlet else P.apply(x)
+    y = assemble(res, P.ndof, parallel.plane_size(n[0], n[1], p), "y")
     assert normwise(y, ref) <= PARITY_TOL
-    g.close()
+    for r in res:  # the three repeated applies agree to rounding
+        assert normwise(r["all"][0], r["y"]) <= 1e-15
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_loopback_dot_owned_dofs(world):
-    g = Group("diffusion", (3, 2, 8), 3, world)
+def test_multirank_dot_owned_dofs(pools, world):
+    vals = pools(world).run("dot", n=(3, 2, 8), p=3)
+    P = bp.Problem("diffusion", 3, 2, 8, 3)
     rng = np.random.default_rng(3)
-    a, b = rng.standard_normal(g.P.ndof), rng.standard_normal(g.P.ndof)
-    xa, xb = g.local(a), g.local(b)
-    vals = g.run(lambda r, s, bar: [g.ops[r].dot(xa[r], xb[r]) for _ in range(4)])
+    a, b = rng.standard_normal(P.ndof), rng.standard_normal(P.ndof)
     ref = float(a @ b)
     for v in vals:
-        # every rank holds the same bits (slot sums in rank order)
-        assert v == vals[0]
+        assert v == vals[0]  # every rank holds the same bits (slot sums in rank order)
         assert abs(v[0] - ref) <= 1e-13 * np.sqrt(float(a @ a) * float(b @ b))
-    g.close()
 
 
 @pytest.mark.parametrize("kind,n,p,world", [("diffusion", (3, 2, 6), 4, 3), ("mass", (2, 3, 4), 3, 2)])
-def test_loopback_diagonal(kind, n, p, world):
-    g = Group(kind, n, p, world, dirichlet=True)
-    outs = g.empty()
-    g.run(lambda r, s, bar: g.ops[r].diagonal(out=outs[r]))
-    ref = g.P.diagonal()
-    ref[g.P.boundary()] = 1.0
-    assert normwise(g.assemble(outs), ref) <= PARITY_TOL
-    g.close()
+def test_multirank_diagonal(pools, kind, n, p, world):
+    res = pools(world).run("diagonal", kind=kind, n=n, p=p)
+    P = bp.Problem(kind, *n, p)
+    ref = P.diagonal()
+    ref[P.boundary()] = 1.0
+    assert normwise(assemble(res, P.ndof, parallel.plane_size(n[0], n[1], p), "d"), ref) <= PARITY_TOL
 
 
 CG_CASES = [
@@ -164,122 +115,68 @@ CG_CASES = [
 
 
 @pytest.mark.parametrize("kind,n,p,world,variant,iters", CG_CASES)
-def test_loopback_cg_matches_oracle(kind, n, p, world, variant, iters):
-    g = Group(kind, n, p, world, dirichlet=True, variant=variant)
-    b = np.random.default_rng(0).standard_normal(g.P.ndof)
-    b[g.P.boundary()] = 0.0
-    bs, xs = g.local(b), g.empty()
-    res = g.run(lambda r, s, bar: cg_solve(g.ops[r], bs[r], iters=iters, out=xs[r], barrier=bar)[1])
-    xr, hr = g.P.pcg(b, iters=iters)
-    for h in res:
-        assert len(h) == len(hr)
-        assert np.array_equal(h, res[0])  # identical scalars on every rank
-        assert np.max(np.abs(h - hr)) <= 1e-8 * hr[0]
-    x = g.assemble(xs)
+def test_multirank_cg_matches_oracle(pools, kind, n, p, world, variant, iters):
+    res = pools(world).run("cg", kind=kind, n=n, p=p, iters=iters, variant=variant)
+    P = bp.Problem(kind, *n, p)
+    b = np.random.default_rng(0).standard_normal(P.ndof)
+    b[P.boundary()] = 0.0
+    xr, hr = P.pcg(b, iters=iters)
+    for r in res:
+        assert len(r["h"]) == len(hr)
+        assert np.array_equal(r["h"], res[0]["h"])  # identical scalars on every rank
+        assert np.max(np.abs(r["h"] - hr)) <= 1e-8 * hr[0]
+        assert r["applies"] == iters
+    x = assemble(res, P.ndof, parallel.plane_size(n[0], n[1], p), "x")
     assert normwise(x, xr) <= 1e-8
-    for op in g.ops:
-        assert op.counters.operator_applies == iters
-    g.close()
 
 
-def test_loopback_cg_rtol_stops_every_rank_together():
-    g = Group("diffusion", (3, 3, 6), 3, 3, dirichlet=True)
-    b = np.random.default_rng(1).standard_normal(g.P.ndof)
-    b[g.P.boundary()] = 0.0
-    bs, xs = g.local(b), g.empty()
-    res = g.run(lambda r, s, bar: cg_solve(g.ops[r], bs[r], iters=200, rtol=1e-6, out=xs[r],
-                                           barrier=bar)[1])
-    _, hr = g.P.pcg(b, iters=200, rtol=1e-6)
-    assert all(len(h) == len(hr) for h in res) and len(hr) < 201
-    g.close()
+def test_multirank_cg_rtol_stops_every_rank_together(pools):
+    res = pools(3).run("cg", kind="diffusion", n=(3, 3, 6), p=3, iters=200, rtol=1e-6, seed=1)
+    P = bp.Problem("diffusion", 3, 3, 6, 3)
+    b = np.random.default_rng(1).standard_normal(P.ndof)
+    b[P.boundary()] = 0.0
+    _, hr = P.pcg(b, iters=200, rtol=1e-6)
+    assert all(len(r["h"]) == len(hr) for r in res) and len(hr) < 201
+    assert all(r["applies"] == len(hr) - 1 for r in res)
 
 
-def test_loopback_matches_single_gpu_bitwise_inside_slabs():
-    """Interior dofs of a slab see exactly the same element contributions in
-    the same kernel as the single-GPU apply; only shared planes add two
-    partial sums in a different order."""
+def test_multirank_matches_single_gpu(pools):
+    """Interior dofs of a slab see the same element contributions as the
+    single-GPU apply; only shared planes add two partial sums in another order."""
     n, p = (3, 3, 8), 4
-    g = Group("diffusion", n, p, 2)
+    res = pools(2).run("apply", kind="diffusion", n=n, p=p)
     single = PAOperator(fem.build_mesh(*n), p)
-    x = np.random.default_rng(9).standard_normal(g.P.ndof)
-    ref = single.apply(dev(x)).cpu().numpy()
-    xs, ys = g.local(x), g.empty()
-    g.run(lambda r, s, bar: g.ops[r].apply(xs[r], out=ys[r]))
-    y = g.assemble(ys)
+    x = np.random.default_rng(7).standard_normal(single.num_dofs)
+    ref = single.apply(torch.as_tensor(x, device="cuda")).cpu().numpy()
+    y = assemble(res, single.num_dofs, parallel.plane_size(n[0], n[1], p), "y")
     assert normwise(y, ref) <= 1e-15
     single.close()
-    g.close()
+
+
+def test_deterministic_multirank_cg_bitwise(pools):
+    """Verification mode across ranks: colour-ordered slabs, rank-ordered
+    reductions — two solves are bit-identical (history and solution)."""
+    kw = dict(kind="diffusion", n=(3, 3, 8), p=4, iters=40, seed=5, deterministic=True)
+    a = pools(3).run("cg", **kw)
+    b = pools(3).run("cg", **kw)
+    for ra, rb in zip(a, b):
+        assert np.array_equal(ra["h"], rb["h"]) and np.array_equal(ra["x"], rb["x"])
+    P = bp.Problem("diffusion", 3, 3, 8, 4)
+    bb = np.random.default_rng(5).standard_normal(P.ndof)
+    bb[P.boundary()] = 0.0
+    _, hr = P.pcg(bb, iters=40)
+    assert np.max(np.abs(a[0]["h"] - hr)) <= 1e-8 * hr[0]
+
+
+def test_deterministic_multirank_apply_bitwise(pools):
+    res = pools(2).run("apply", kind="diffusion", n=(4, 3, 6), p=3, deterministic=True, reps=4)
+    for r in res:
+        for y in r["all"]:
+            assert np.array_equal(y, r["all"][0])
 
 
 def test_plane_capacity_is_checked():
-    comms = Comm.loopback(2, 10)
-    with pytest.raises(ValueError, match="do(es)? not match"):
-        PAOperator(fem.build_mesh(3, 3, 4), 3, comm=comms[0])
-    for c in comms:
-        c.close()
-
-
-# -- two processes, CUDA IPC mailboxes -------------------------------------------------
-
-WORKER = r"""
-import os, sys, numpy as np, torch, torch.distributed as dist
-sys.path.insert(0, os.environ["FK_ROOT"]); sys.path.insert(0, os.path.join(os.environ["FK_ROOT"], "tests"))
-from paper_2603_09038_b200 import Comm, PAOperator, cg_solve, fem, parallel
-rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-dist.init_process_group("gloo", init_method="tcp://127.0.0.1:" + os.environ["FK_PORT"], rank=rank, world_size=world)
-torch.cuda.set_device(0)
-n, p = (3, 2, 6), 4
-comm = Comm(rank, world, 0, transport="p2p")
-s = torch.cuda.Stream()
-op = PAOperator(fem.build_mesh(*n), p, dirichlet=True, comm=comm, stream=s)
-z0, z1 = comm.slab(n[2])
-lo, hi = parallel.local_dof_range(n[0], n[1], p, z0, z1)
-rng = np.random.default_rng(0)
-x = rng.standard_normal((n[0]*p+1)*(n[1]*p+1)*(n[2]*p+1))
-with torch.cuda.stream(s):
-    xl = torch.as_tensor(x[lo:hi], device="cuda")
-    y = op.apply(xl)
-    b = op.set_essential(xl.clone(), 0.0)
-    xs, h = cg_solve(op, b, iters=25)
-    d = op.dot(xl, xl)
-s.synchronize()
-np.savez(os.environ["FK_OUT"] + f"_{rank}.npz", y=y.cpu().numpy(), x=xs.cpu().numpy(), h=h, d=d, lo=lo, hi=hi)
-dist.barrier()
-op.close(); comm.close()
-dist.destroy_process_group()
-"""
-
-
-def test_two_process_ipc_p2p(tmp_path):
-    n, p, world = (3, 2, 6), 4, 2
-    script = tmp_path / "worker.py"
-    script.write_text(WORKER)
-    port = str(29600 + os.getpid() % 300)
-    procs = []
-    for r in range(world):
-        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), FK_ROOT=ROOT, FK_PORT=port,
-                   FK_OUT=str(tmp_path / "out"))
-        procs.append(subprocess.Popen([sys.executable, str(script)], env=env,
-                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
-    for pr in procs:
-        out, _ = pr.communicate(timeout=300)
-        assert pr.returncode == 0, out.decode()[-3000:]
-    P = bp.Problem("diffusion", *n, p)
-    x = np.random.default_rng(0).standard_normal(P.ndof)
-    ess = P.boundary()
-    res = [np.load(tmp_path / f"out_{r}.npz") for r in range(world)]
-    y = np.zeros(P.ndof)
-    xs = np.zeros(P.ndof)
-    for r in res:
-        y[int(r["lo"]):int(r["hi"])] = r["y"]
-        xs[int(r["lo"]):int(r["hi"])] = r["x"]
-    plane = parallel.plane_size(n[0], n[1], p)
-    assert np.array_equal(res[0]["y"][-plane:], res[1]["y"][:plane])
-    assert normwise(y, P.constrained_apply(x, ess)) <= PARITY_TOL
-    b = x.copy()
-    b[ess] = 0.0
-    xr, hr = P.pcg(b, iters=25)
-    for r in res:
-        assert len(r["h"]) == len(hr) and np.max(np.abs(r["h"] - hr)) <= 1e-8 * hr[0]
-        assert abs(float(r["d"]) - float(x @ x)) <= 1e-12 * float(x @ x)
-    assert normwise(xs, xr) <= 1e-8
+    comm = Comm(0, 1, 0, transport="p2p", plane_cap=10)
+    with pytest.raises(ValueError, match="does not match"):
+        PAOperator(fem.build_mesh(3, 3, 4), 3, comm=comm)
+    comm.close()
