@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--mixed", action="store_true",
                     help="acoustic-gravity FusedPA block apply (paper Table VII: H1 p=4 x L2 p=3, "
                          "q=5, ~540 M dofs; SURVEY.md §8f) + an RK4 step")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="verification mode: colour-ordered elements, bitwise reproducible applies")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="z-slab exchange for N>1: peer-memory mailboxes (default) or NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -383,7 +385,8 @@ def run_ours(a):
     q = a.q or p + 2
     n = a.n or (54 if p == 4 else SWEEP_N.get(p, 54))
     mesh = build_mesh(n, n, n * world)
-    op = PAOperator(mesh, p, q, kind=a.kind, variant=a.variant, comm=comm)
+    op = PAOperator(mesh, p, q, kind=a.kind, variant=a.variant, comm=comm,
+                    deterministic=a.deterministic)
     rng = np.random.default_rng(rank)
     x = torch.as_tensor(rng.standard_normal(op.num_dofs), device="cuda")
     y = torch.empty_like(x)
@@ -417,7 +420,8 @@ def run_ours(a):
         # weak-scaling reference: the same per-rank slab alone on this GPU (no
         # exchange), timed the same way, before the multi-rank run
         trace("solo slab")
-        solo = PAOperator(build_mesh(n, n, n), p, q, kind=a.kind, variant=a.variant)
+        solo = PAOperator(build_mesh(n, n, n), p, q, kind=a.kind, variant=a.variant,
+                          deterministic=a.deterministic)
         for _ in range(max(3, a.warmup)):
             solo.apply(x, out=y)
         barrier()
@@ -511,6 +515,7 @@ def run_ours(a):
             "impl_config": {
                 "variant": op.variant, "cfg": op.info.cfg, "dofs_per_gpu": op.num_dofs,
                 "transport": a.transport if world > 1 else None,
+                "deterministic": a.deterministic,
                 "l2": ((f"inputs larger than L2 ({op.bytes_per_apply / 1e9:.2f} GB moved "
                         "per apply, no flush needed)") if op.bytes_per_apply > 126e6 else
                        "small config: L2-resident between steps (not a bandwidth number)"),
@@ -620,7 +625,8 @@ def run_cg(a):
     single_ms = None
     if world > 1 and (scaling == "weak" or rank == 0):
         solo_dims = (dims[0], dims[1], dims[2] // world) if scaling == "weak" else dims
-        solo = PAOperator(build_mesh(*solo_dims), p, kind="diffusion", dirichlet=True, variant=a.variant)
+        solo = PAOperator(build_mesh(*solo_dims), p, kind="diffusion", dirichlet=True, variant=a.variant,
+                          deterministic=a.deterministic)
         bs = torch.as_tensor(np.random.default_rng(rank).standard_normal(solo.num_dofs), device="cuda")
         solo.set_essential(bs, 0.0)
         single_ms, _ = solve_ms(solo, bs)
@@ -630,7 +636,8 @@ def run_cg(a):
     if world > 1:
         dist.barrier()
         single_ms = max_over_ranks(single_ms or 0.0)
-    op = PAOperator(build_mesh(*dims), p, kind="diffusion", dirichlet=True, variant=a.variant, comm=comm)
+    op = PAOperator(build_mesh(*dims), p, kind="diffusion", dirichlet=True, variant=a.variant, comm=comm,
+                    deterministic=a.deterministic)
     b = torch.as_tensor(np.random.default_rng(rank).standard_normal(op.num_dofs), device="cuda")
     op.set_essential(b, 0.0)
     sampler = ClockSampler(local)
@@ -657,7 +664,8 @@ def run_cg(a):
                        "mesh": list(dims), "p": p, "q": p + 2, "iterations": iters,
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
             "impl_config": {"variant": op.variant, "cfg": op.info.cfg, "dofs_per_gpu": op.num_dofs,
-                            "transport": a.transport if world > 1 else None},
+                            "transport": a.transport if world > 1 else None,
+                            "deterministic": a.deterministic},
             "cpu_baseline": cpu,
             "clocks": sampler.summary(),
         }

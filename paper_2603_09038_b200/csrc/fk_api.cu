@@ -220,7 +220,9 @@ int launch_all(fk_op* op, const double* x, double* y, cudaStream_t s) {
       FK_TRY(launch_range(op, x, y, op->colour_off[c], op->colour_off[c + 1] - op->colour_off[c], s));
     return FK_OK;
   }
-  op->kern->launch(view(op), x, y, op->blocks, s);
+  fk::OpView v = view(op);
+  if (op->qf_on) v.qf = op->qf_part + (size_t)op->qf_seg++ * op->max_blocks;
+  op->kern->launch(v, x, y, op->blocks, s);
   FK_CUDA(cudaGetLastError());
   return FK_OK;
 }
@@ -239,6 +241,7 @@ int launch_range(fk_op* op, const double* x, double* y, int64_t e0, int64_t ne, 
   v.e0 = e0;
   if (v.ebits) v.ebits += e0 * op->ms;
   v.nel = (int)ne;
+  if (op->qf_on) v.qf = op->qf_part + (size_t)op->qf_seg++ * op->max_blocks;
   const int64_t nb = (ne + op->kern->E - 1) / op->kern->E;
   const int blocks =
       (int)std::max<int64_t>(1, op->kern->persist ? std::min<int64_t>(nb, op->max_blocks) : nb);
@@ -309,9 +312,10 @@ static int preload_kernels(const fk_op* op) {
                       reinterpret_cast<const void*>(&fk::cg_init_kernel),
                       reinterpret_cast<const void*>(&fk::cg_start_kernel),
                       reinterpret_cast<const void*>(&fk::cg_alpha_kernel),
-                      reinterpret_cast<const void*>(&fk::cg_update_kernel),
+                      reinterpret_cast<const void*>(&fk::cg_residual_kernel),
                       reinterpret_cast<const void*>(&fk::cg_finish_kernel),
-                      reinterpret_cast<const void*>(&fk::cg_dir_kernel),
+                      reinterpret_cast<const void*>(&fk::cg_step_kernel),
+                      reinterpret_cast<const void*>(&fk::qf_sum_kernel),
                       reinterpret_cast<const void*>(&fk::recip_kernel)};
   cudaFuncAttributes a;
   for (const void* k : ks) FK_CUDA(cudaFuncGetAttributes(&a, k));
@@ -559,6 +563,7 @@ int fk_op_destroy(fk_op* op) {
   cudaFree(op->partials);
   cudaFree(op->counter);
   cudaFree(op->hist);
+  cudaFree(op->qf_part);
   cudaFree(op->halo);
   if (op->comm_stream) cudaStreamDestroy(op->comm_stream);
   if (op->ev_bnd) cudaEventDestroy(op->ev_bnd);
@@ -791,27 +796,40 @@ int fk_dot(fk_op* op, const double* a, const double* b, double* host_out) {
   return FK_OK;
 }
 
-// One CG iteration, enqueued on stream s (capturable).
+// One CG iteration, enqueued on stream s (capturable).  With an EO / MF
+// kernel, p.Ap comes out of the apply itself (per-CTA quadratic-form
+// partials, summed in fixed order); otherwise a dot pass over p and Ap.
 static int cg_iteration(fk_op* op, double* x, cudaStream_t s) {
   const int64_t n = op->ndof, n0 = fk::owned_begin(op);
   double* r = op->work;
-  double* z = r + n;
-  double* p = z + n;
+  double* p = r + 2 * n;
   double* Ap = p + n;
   double* dinv = Ap + n;
   int* iscal = reinterpret_cast<int*>(op->scal + 16);
   const int rb = red_blocks(op);
-  FK_TRY(apply_full(op, p, Ap, s));
-  fk::dot_kernel<<<rb, fk::kRedThreads, 0, s>>>(p, Ap, n0, n, op->partials, op->counter,
-                                                op->scal + fk::S_DEN);
+  const bool qf = op->kern->qf && op->qf_part != nullptr;
+  if (qf) {
+    FK_CUDA(cudaMemsetAsync(op->qf_part, 0, sizeof(double) * 8 * op->max_blocks, s));
+    op->qf_on = true;
+    op->qf_seg = 0;
+  }
+  const int rc = apply_full(op, p, Ap, s);
+  op->qf_on = false;
+  FK_TRY(rc);
+  if (qf)
+    fk::qf_sum_kernel<<<1, fk::kRedThreads, 0, s>>>(op->qf_part, (int64_t)op->qf_seg * op->max_blocks,
+                                                   op->scal + fk::S_DEN);
+  else
+    fk::dot_kernel<<<rb, fk::kRedThreads, 0, s>>>(p, Ap, n0, n, op->partials, op->counter,
+                                                  op->scal + fk::S_DEN);
   if (op->comm) FK_TRY(fk::allreduce_scalar(op, op->scal + fk::S_DEN, s));
   fk::cg_alpha_kernel<<<1, 1, 0, s>>>(op->scal, iscal);
-  fk::cg_update_kernel<<<rb, fk::kRedThreads, 0, s>>>(x, r, z, p, Ap, dinv, n, n0, op->scal, iscal,
-                                                      op->partials, op->counter + 1,
-                                                      op->scal + fk::S_BN);
+  fk::cg_residual_kernel<<<rb, fk::kRedThreads, 0, s>>>(r, Ap, dinv, n, n0, op->scal, iscal,
+                                                        op->partials, op->counter + 1,
+                                                        op->scal + fk::S_BN);
   if (op->comm) FK_TRY(fk::allreduce_scalar(op, op->scal + fk::S_BN, s));
   fk::cg_finish_kernel<<<1, 1, 0, s>>>(op->scal, iscal, op->hist);
-  fk::cg_dir_kernel<<<grid_for(n, 256, op->num_sms), 256, 0, s>>>(p, z, n, op->scal, iscal);
+  fk::cg_step_kernel<<<grid_for(n, 256, op->num_sms), 256, 0, s>>>(x, p, r, dinv, n, op->scal, iscal);
   FK_CUDA(cudaGetLastError());
   return FK_OK;
 }
@@ -830,6 +848,8 @@ int fk_cg_prepare(fk_op* op, int iters) {
     op->hist_cap = iters + 1;
   }
   if (op->cg_stream == nullptr) FK_CUDA(cudaStreamCreateWithFlags(&op->cg_stream, cudaStreamNonBlocking));
+  if (op->qf_part == nullptr && op->max_blocks > 0)
+    FK_CUDA(cudaMalloc(&op->qf_part, sizeof(double) * 8 * op->max_blocks));
   return FK_OK;
 }
 
@@ -861,7 +881,7 @@ int fk_cg_solve(fk_op* op, const double* b, double* x, int iters, double rtol, d
   fk::recip_kernel<<<grid_for(n, 256, op->num_sms), 256, 0, s>>>(dinv, z, n);
   const int64_t n0 = fk::owned_begin(op);
   fk::cg_init_kernel<<<red_blocks(op), fk::kRedThreads, 0, s>>>(
-      b, x, r, z, p, dinv, n, n0, op->partials, op->counter + 2, op->scal + fk::S_NOM);
+      b, x, r, p, dinv, n, n0, op->partials, op->counter + 2, op->scal + fk::S_NOM);
   if (op->comm) FK_TRY(fk::allreduce_scalar(op, op->scal + fk::S_NOM, s));
   fk::cg_start_kernel<<<1, 1, 0, s>>>(op->scal, iscal, op->hist, rtol);
   FK_CUDA(cudaGetLastError());

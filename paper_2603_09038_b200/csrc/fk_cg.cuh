@@ -1,10 +1,15 @@
 // fk_cg.cuh — device-resident Jacobi-PCG pieces (MFEM CGSolver semantics).
 //
 // All scalars stay on the device; one iteration is
-//   apply(p -> Ap) ; den = p.Ap ; alpha = nom/den ;
-//   x += alpha p ; r -= alpha Ap ; z = dinv r ; bn = r.z   (one fused pass)
-//   hist[it] = sqrt(bn) ; beta = bn/nom ; nom = bn ; p = z + beta p
+//   apply(p -> Ap), with den = p.Ap formed inside the fused kernel as the sum
+//     of element quadratic forms g^T D g at the quadrature points (EO bodies;
+//     other kernels: a dot pass) ; alpha = nom/den
+//   r -= alpha Ap ; bn = r.(dinv r)                   (one pass, z not stored)
+//   hist[it] = sqrt(bn) ; beta = bn/nom ; nom = bn
+//   x += alpha p ; p = dinv r + beta p                (one pass)
 // and is captured once into a CUDA graph that is replayed `iters` times.
+// Vector traffic per iteration: 32 + 48 B/dof (was 16 + 64 + 24 with the
+// separate dot, the stored z and the x update in the residual pass).
 // Reductions are deterministic: fixed grid, fixed per-block order, the last
 // block to finish sums the block partials in index order.
 #pragma once
@@ -14,7 +19,7 @@
 namespace fk {
 
 enum ScalarSlot { S_NOM = 0, S_DEN = 1, S_BN = 2, S_STOP = 3, S_ALPHA = 4, S_BETA = 5, S_DOT = 6 };
-enum IntSlot { I_DONE = 0, I_IT = 1 };
+enum IntSlot { I_DONE = 0, I_IT = 1, I_ACT = 2 };  // I_ACT: this iteration updates x, r
 
 constexpr int kRedThreads = 256;
 
@@ -69,22 +74,37 @@ __global__ void __launch_bounds__(kRedThreads) dot_kernel(const double* __restri
   reduce_finish(s, partials, counter, out);
 }
 
-// x = 0, r = b, z = dinv*b, p = z; partial r.z over [n0, n1)
+// x = 0, r = b, p = dinv*b; partial r.(dinv r) over [n0, n1)
 __global__ void __launch_bounds__(kRedThreads) cg_init_kernel(
     const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r,
-    double* __restrict__ z, double* __restrict__ p, const double* __restrict__ dinv, int64_t n,
-    int64_t n0, double* partials, unsigned* counter, double* out) {
+    double* __restrict__ p, const double* __restrict__ dinv, int64_t n, int64_t n0,
+    double* partials, unsigned* counter, double* out) {
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)kRedThreads + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * kRedThreads) {
     const double bi = b[i], zi = dinv[i] * bi;
     x[i] = 0.0;
     r[i] = bi;
-    z[i] = zi;
     p[i] = zi;
     if (i >= n0) s = fma(bi, zi, s);
   }
   reduce_finish(s, partials, counter, out);
+}
+
+// *out = sum of the n per-CTA quadratic-form partials, fixed order (one CTA)
+__global__ void __launch_bounds__(kRedThreads) qf_sum_kernel(const double* __restrict__ part,
+                                                             int64_t n, double* out) {
+  __shared__ double sw[kRedThreads / 32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += kRedThreads) s += part[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) t += sw[w];
+    *out = t;
+  }
 }
 
 __global__ void cg_start_kernel(double* scal, int* iscal, double* hist, double rtol) {
@@ -98,6 +118,7 @@ __global__ void cg_start_kernel(double* scal, int* iscal, double* hist, double r
 }
 
 __global__ void cg_alpha_kernel(double* scal, int* iscal) {
+  iscal[I_ACT] = 0;
   if (iscal[I_DONE]) return;
   const double den = scal[S_DEN];
   if (den == 0.0) {  // MFEM breaks on p.Ap == 0 (no 0/0 update)
@@ -105,26 +126,22 @@ __global__ void cg_alpha_kernel(double* scal, int* iscal) {
     return;
   }
   scal[S_ALPHA] = scal[S_NOM] / den;
+  iscal[I_ACT] = 1;
 }
 
-// x += alpha p ; r -= alpha Ap ; z = dinv r ; partial r.z over [n0, n)
-__global__ void __launch_bounds__(kRedThreads) cg_update_kernel(
-    double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
-    const double* __restrict__ p, const double* __restrict__ Ap, const double* __restrict__ dinv,
+// r -= alpha Ap ; partial r.(dinv r) over [n0, n)
+__global__ void __launch_bounds__(kRedThreads) cg_residual_kernel(
+    double* __restrict__ r, const double* __restrict__ Ap, const double* __restrict__ dinv,
     int64_t n, int64_t n0, const double* scal, const int* iscal, double* partials,
     unsigned* counter, double* out) {
-  if (iscal[I_DONE]) return;  // uniform across the grid
+  if (!iscal[I_ACT]) return;  // uniform across the grid
   const double alpha = scal[S_ALPHA];
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)kRedThreads + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * kRedThreads) {
-    const double pi = p[i];
-    x[i] = fma(alpha, pi, x[i]);
     const double ri = fma(-alpha, Ap[i], r[i]);
-    const double zi = dinv[i] * ri;
     r[i] = ri;
-    z[i] = zi;
-    if (i >= n0) s = fma(ri, zi, s);
+    if (i >= n0) s = fma(ri, dinv[i] * ri, s);
   }
   reduce_finish(s, partials, counter, out);
 }
@@ -140,13 +157,19 @@ __global__ void cg_finish_kernel(double* scal, int* iscal, double* hist) {
   if (bn <= scal[S_STOP]) iscal[I_DONE] = 1;
 }
 
-__global__ void cg_dir_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
-                              const double* scal, const int* iscal) {
-  if (iscal[I_DONE]) return;
-  const double beta = scal[S_BETA];
+// x += alpha p (this iteration ran) ; p = dinv r + beta p (unless converged)
+__global__ void cg_step_kernel(double* __restrict__ x, double* __restrict__ p,
+                               const double* __restrict__ r, const double* __restrict__ dinv,
+                               int64_t n, const double* scal, const int* iscal) {
+  if (!iscal[I_ACT]) return;
+  const double alpha = scal[S_ALPHA], beta = scal[S_BETA];
+  const bool dir = !iscal[I_DONE];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], z[i]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double pi = p[i];
+    x[i] = fma(alpha, pi, x[i]);
+    if (dir) p[i] = fma(beta, pi, dinv[i] * r[i]);
+  }
 }
 
 __global__ void recip_kernel(double* __restrict__ out, const double* __restrict__ in, int64_t n) {

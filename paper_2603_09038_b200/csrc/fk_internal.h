@@ -20,6 +20,7 @@ struct KernelEntry {
   int E = 0, T = 0;
   bool persist = true;  // persistent grid (batches strided over CTAs) or one batch per CTA
   bool structured = false;  // ids from the closed-form box restriction (no user gather map)
+  bool qf = false;          // can accumulate the element quadratic form (OpView::qf)
   size_t smem = 0;
   const void* func = nullptr;
   const void* diag_func = nullptr;  // the assembled-diagonal kernel of this (d, q, nc)
@@ -41,6 +42,7 @@ struct OpView {
   // of this launch within the rank's slab
   int nx, ny, p;
   int64_t npx, npy, e0;
+  double* qf = nullptr;  // QF-capable kernels: per-CTA quadratic-form partials
 };
 
 // Host mirror of GlobalLayout (pa_common.cuh): padded per-element strides.
@@ -181,6 +183,11 @@ struct fk_op {
   unsigned* counter = nullptr;
   double* hist = nullptr;
   int hist_cap = 0;
+  // CG: p.Ap as the fused kernel's quadratic form (per-CTA partials of up to 8
+  // launches per apply: the colour launches / the overlapped layer ranges)
+  double* qf_part = nullptr;
+  bool qf_on = false;
+  int qf_seg = 0;
   // multi-rank
   fk_comm* comm = nullptr;
   double* halo = nullptr;  // receive buffers (2 planes)

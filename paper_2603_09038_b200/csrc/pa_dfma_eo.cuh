@@ -360,9 +360,15 @@ struct DfmaEoBody {
   // T2 (a, b, k) + D -> W (a, b, k): thread per line (a, b); W region sw.
   // MF: D computed from the 1D weights and the element Jacobian, in the PA
   // setup's operation order (fk_setup.cuh pa_data_kernel), so bit-identical.
+  // qacc (optional): += sum over this thread's quadrature points of g^T D g,
+  // g the reference gradients (BP3) / values (BP1) at the point — the element
+  // quadratic form x_e^T A_e x_e, i.e. p.Ap of a CG iteration without a pass
+  // over the assembled vectors (fk_api.cu cg_iteration)
+  static constexpr bool QF_OK = true;
   template <bool MF = false>
   __device__ __forceinline__ static void stage_c(const Tab& tb, int it, const double* s0,
-                                                 const double* db, double* sw, int ne, double*) {
+                                                 const double* db, double* sw, int ne, double*,
+                                                 double* qacc = nullptr) {
     const double* tab = tb.t[PP ? (it & 1) : 0];
     constexpr int N = E * Q * Q;
     constexpr int NIT = (N + T - 1) / T;
@@ -402,6 +408,7 @@ struct DfmaEoBody {
             g1[c] = fma(d12, a2, fma(d11, a1, d01 * a0));
             g2[c] = fma(d22, a2, fma(d12, a1, d02 * a0));
           }
+          if (qacc) *qacc = fma(a2, g2[c], fma(a1, g1[c], fma(a0, g0[c], *qacc)));
         }
         double w[D], w1[D];
         contract_pair<SR, Q, D, +1>(tab + Tab::TBT, g0, g1, w, w1);
@@ -416,7 +423,11 @@ struct DfmaEoBody {
         double g[Q], w[D];
         contract_eo<D, Q, +1>(tab + Tab::TB, tin[0], g);
 #pragma unroll
-        for (int c = 0; c < Q; ++c) g[c] *= MF ? (tb.mfw[c] * wab) * tb.mfc[0] : pe[c * Q * Q];
+        for (int c = 0; c < Q; ++c) {
+          const double a0 = g[c];
+          g[c] *= MF ? (tb.mfw[c] * wab) * tb.mfc[0] : pe[c * Q * Q];
+          if (qacc) *qacc = fma(a0, g[c], *qacc);
+        }
         contract_eo<Q, D, +1>(tab + Tab::TBT, g, w);
 #pragma unroll
         for (int k = 0; k < D; ++k) sw[LW::at(e, 0, a, b, k)] = w[k];

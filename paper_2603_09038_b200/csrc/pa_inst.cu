@@ -36,7 +36,7 @@ void div_magic(int d, unsigned& m, int& s) {
 }
 
 StructIds struct_ids(const OpView& v) {
-  StructIds sid{v.nx, v.ny, v.p, (int)v.npx, (int)v.npy, (long long)v.e0, 0u, 0u, 0, 0};
+  StructIds sid{v.nx, v.ny, v.p, (int)v.npx, (int)v.npy, (long long)v.e0, 0u, 0u, 0, 0, v.qf};
   if (v.nx > 0 && v.ny > 0) {
     div_magic(v.nx, sid.mnx, sid.snx);
     div_magic(v.ny, sid.mny, sid.sny);
@@ -77,6 +77,7 @@ KernelEntry entry(int variant, int cfg) {
   k.T = Body::T;
   k.persist = PERSIST;
   k.structured = GM == 1;
+  k.qf = HasQf<Body>::value && PERSIST;
   k.smem = PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES;
   k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>);
   k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>;

@@ -62,6 +62,17 @@ struct StructIds {
   long long e0;
   unsigned mnx, mny;
   int snx, sny;
+  double* qf;  // non-null: CTA b writes its share of sum_e x_e^T A_e x_e to qf[b]
+};
+
+// bodies whose stage C can accumulate the element quadratic form (QF_OK)
+template <class B, class = void>
+struct HasQf {
+  static constexpr bool value = false;
+};
+template <class B>
+struct HasQf<B, decltype((void)B::QF_OK)> {
+  static constexpr bool value = B::QF_OK;
 };
 
 __device__ __forceinline__ int fast_div(int n, unsigned m, int s) {
@@ -294,6 +305,9 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   wait_g(0);
   issue_x(blockIdx.x, 0, xb);
 
+  // element quadratic form (CG's p.Ap): per-thread partial in a register
+  double qacc = 0.0;
+  double* const qptr = sid.qf ? &qacc : nullptr;
   auto run_batch = [&](int b, int it) {
     const int gslot = it % NG;
     double* xcur = SX ? xb : xb + (it & 1) * E * XS;
@@ -323,7 +337,17 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     }
     Body::stage_b(tb, it, s1, s0, ne, ex);
     __syncthreads();
-    if constexpr (MF) {
+    if constexpr (HasQf<Body>::value) {
+      if constexpr (MF) {
+        Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex, qptr);
+      } else if constexpr (DG) {
+        Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex, qptr);
+      } else {
+        mbar_wait(bar_d, ph_d);
+        ph_d ^= 1u;
+        Body::stage_c(tb, it, s0, db, sw, ne, ex, qptr);
+      }
+    } else if constexpr (MF) {
       Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex);
     } else if constexpr (DG) {
       Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex);
@@ -358,6 +382,20 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     // one batch per CTA: no loop, so the compiler has nothing to hoist the
     // basis-table loads out of (co-resident CTAs overlap load and compute)
     run_batch(blockIdx.x, 0);
+  }
+  if constexpr (HasQf<Body>::value) {
+    if (sid.qf) {  // CTA partial of the quadratic form, fixed reduction order
+      __shared__ double qw[(T + 31) / 32];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) qacc += __shfl_down_sync(0xffffffffu, qacc, o);
+      if ((threadIdx.x & 31) == 0) qw[threadIdx.x >> 5] = qacc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (T + 31) / 32; ++w) s += qw[w];
+        sid.qf[blockIdx.x] = s;
+      }
+    }
   }
 }
 
