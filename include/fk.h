@@ -207,7 +207,8 @@ int fk_op_time_apply(fk_op* op, const double* x_dev, double* y_dev, int reps,
  * D = dmat = w|J| J^-1 (9 components per point, :137-144) is read once per
  * element for both blocks.  Compiled spaces: order_u = order_p - 1,
  * num_quad_1d = order_p + 1, order_p = 2..8 (the reference default 4/3/5).
- * No absorbing faces or surface gravity (:400-440).
+ * Boundary terms (:400-470): absorbing lateral faces (in fk_mix_apply and
+ * the RK4 driver), the free-surface lumped mass, the bottom-face load.
  * ------------------------------------------------------------------------- */
 typedef struct fk_mix fk_mix;
 
@@ -228,6 +229,10 @@ typedef struct fk_mix_desc {
                                   operator.py:280-286); 0: FusedPA / PA */
   int device;
   void* stream;                /* cudaStream_t */
+  int absorbing;               /* 1: impedance term on the lateral (x, y) faces inside apply
+                                  (BlockOperator absorbing=True, _apply_absorbing :432-439) */
+  double surface_gravity;      /* > 0: free-surface lumped mass on the top face (:268-276);
+                                  0: none */
 } fk_mix_desc;
 
 typedef struct fk_mix_info {
@@ -251,6 +256,17 @@ int fk_mix_mass_inverse(fk_mix* m, const double* ru, const double* rp, double* u
 /* `steps` classical RK4 steps of [u,p]' = Minv(-A [u,p]) in place (rk4_step,
  * operator.py:506-531, no forcing); four fused applies per step. */
 int fk_mix_rk4(fk_mix* m, double* u, double* p, double dt, int steps);
+/* `steps` = 1 forced RK4 step: [u,p]' = Minv(-A [u,p] + f(t)) (rk4_step with
+ * forcing, operator.py:506-531).  f0, fh, f1: device [u | p] vectors (3 nel
+ * du^3 + ndof_p doubles) of the forcing at t, t + dt/2 and t + dt (NULL: 0). */
+int fk_mix_rk4_forced(fk_mix* m, double* u, double* p, double dt, const double* f0,
+                      const double* fh, const double* f1);
+/* BlockOperator.bottom_face_load (:441-460): load = sum over bottom faces of
+ * area * M2d @ vals_f, M2d = kron(m1, m1), m1 = Bp^T W Bp.  vals: device,
+ * (nx*ny, (order_p+1)^2) profile values at each bottom face's nodes (first
+ * in-plane index fastest, faces x-fastest); load: device ndof_p (overwritten). */
+int fk_mix_bottom_load(fk_mix* m, const double* vals, double* load);
+
 /* parity hooks: lumped diagonals (device copies) and restriction rows (host int64) */
 int fk_mix_lumped(fk_mix* m, double* lump_u, double* lump_p);
 int fk_mix_restriction(fk_mix* m, int64_t* host_out);

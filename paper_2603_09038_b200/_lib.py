@@ -52,7 +52,8 @@ EXPORTS = (
     "fk_comm_destroy",
     "fk_op_time_apply",
     "fk_mix_create", "fk_mix_setup", "fk_mix_destroy", "fk_mix_get_info", "fk_mix_apply",
-    "fk_mix_fused_normal", "fk_mix_mass_inverse", "fk_mix_rk4", "fk_mix_lumped",
+    "fk_mix_fused_normal", "fk_mix_mass_inverse", "fk_mix_rk4", "fk_mix_rk4_forced",
+    "fk_mix_bottom_load", "fk_mix_lumped",
     "fk_mix_restriction", "fk_mix_time_apply",
 )
 
@@ -119,6 +120,8 @@ class FkMixDesc(ctypes.Structure):
         ("matrix_free", ctypes.c_int),
         ("device", ctypes.c_int),
         ("stream", ctypes.c_void_p),
+        ("absorbing", ctypes.c_int),
+        ("surface_gravity", ctypes.c_double),
     ]
 
 
@@ -197,6 +200,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "fk_mix_fused_normal": (i, [vp, vp, vp]),
         "fk_mix_mass_inverse": (i, [vp, vp, vp, vp, vp]),
         "fk_mix_rk4": (i, [vp, vp, vp, d, i]),
+        "fk_mix_rk4_forced": (i, [vp, vp, vp, d, vp, vp, vp]),
+        "fk_mix_bottom_load": (i, [vp, vp, vp]),
         "fk_mix_lumped": (i, [vp, vp, vp]),
         "fk_mix_restriction": (i, [vp, ctypes.POINTER(i64)]),
         "fk_mix_time_apply": (i, [vp, vp, vp, vp, vp, i, pd, pd]),

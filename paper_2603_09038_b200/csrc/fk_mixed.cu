@@ -131,7 +131,7 @@ __global__ void mix_minv_kernel(double* __restrict__ ku, const double* __restric
 }
 
 // One fused RK4 stage update (rk4_step, operator.py:506-531) on [u | p]:
-//   k    = (-r) / lump                      (rhs negation + apply_mass_inverse)
+//   k    = ((-r) + f) / lump                (rhs negation, forcing, apply_mass_inverse)
 //   acc' = (first ? y : acc) + c_acc * k    (the final lincomb, accumulated in
 //                                            the reference's left-to-right order)
 //   ynext = y + c_next * k                  (next stage state; skipped if c_next == 0)
@@ -140,16 +140,111 @@ __global__ void mix_rk4_stage_kernel(const double* __restrict__ r, const double*
                                      int64_t nu, int64_t nel_du3, const double* __restrict__ lump_p,
                                      const double* y, const double* acc_in, double* acc_out,
                                      double* __restrict__ ynext, double c_acc, double c_next,
-                                     int first, int64_t n) {
+                                     int first, int64_t n, const double* __restrict__ f) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     // u is (3, nel, du^3): its lumped entry is lump_u[t - r nel du^3] (no 64-bit modulo)
     const double lump = t < nu ? lump_u[t - (t >= nel_du3 ? (t >= 2 * nel_du3 ? 2 : 1) : 0) * nel_du3]
                                : lump_p[t - nu];
-    const double k = (-r[t]) / lump;
+    const double k = (f ? __dadd_rn(-r[t], f[t]) : -r[t]) / lump;
     const double yt = y[t];
     acc_out[t] = __dadd_rn(first ? yt : acc_in[t], __dmul_rn(c_acc, k));
     if (c_next != 0.0) ynext[t] = __dadd_rn(yt, __dmul_rn(c_next, k));
+  }
+}
+
+// ---- boundary terms (operator.py:400-470) --------------------------------------
+// Face tables: 1D consistent face mass m1 = Bp^T W Bp (dp x dp) and its row
+// sums l1 = Bp^T w; the 2D face mass is kron(m1, m1), the face lump kron(l1, l1)
+// (_init_boundary_terms :420-427).  Face node (a, b): first in-plane index
+// fastest (_face_local_indices :201-210).
+struct FaceTabs {
+  double m1[81];
+  double l1[9];
+};
+
+// element-local node of face node (a, b) on face (axis, side)
+__device__ __forceinline__ int face_node(int axis, int side, int d, int a, int b) {
+  const int lay = side ? d - 1 : 0;
+  return axis == 0 ? lay + d * (a + d * b) : axis == 1 ? a + d * (lay + d * b) : a + d * (b + d * lay);
+}
+
+// Absorbing lateral faces (_apply_absorbing :432-439):
+//   out_p[face] += cs * (area / Z_e) * (kron(m1, m1) p_face),  Z_e = rho sqrt(1/(rho kinv)).
+// Faces in blocks: x-low, x-high (ny nz each), y-low, y-high (nx nz each); one
+// thread per (face, node).
+__global__ void mix_absorb_kernel(const __grid_constant__ FaceTabs ft, double* __restrict__ out_p,
+                                  const double* __restrict__ p, const int* __restrict__ gids,
+                                  int64_t gs, const double* __restrict__ rho,
+                                  const double* __restrict__ kinv, int nx, int ny, int nz, int d,
+                                  double area_x, double area_y, double cs) {
+  const int64_t fx = (int64_t)ny * nz, fy = (int64_t)nx * nz, nf = 2 * (fx + fy);
+  const int d2 = d * d;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nf * d2;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t f = t / d2;
+    const int node = (int)(t - f * d2), a = node % d, b = node / d;
+    int axis, side;
+    int64_t e;
+    if (f < 2 * fx) {
+      axis = 0;
+      side = (int)(f / fx);
+      f -= side * fx;
+      e = (side ? nx - 1 : 0) + (int64_t)nx * (f % ny + (int64_t)ny * (f / ny));
+    } else {
+      f -= 2 * fx;
+      axis = 1;
+      side = (int)(f / fy);
+      f -= side * fy;
+      e = f % nx + (int64_t)nx * ((side ? ny - 1 : 0) + (int64_t)ny * (f / nx));
+    }
+    const int* g = gids + e * gs;
+    double acc = 0.0;
+    for (int bb = 0; bb < d; ++bb) {
+      double row = 0.0;
+      for (int aa = 0; aa < d; ++aa) row = fma(ft.m1[a * d + aa], p[g[face_node(axis, side, d, aa, bb)]], row);
+      acc = fma(ft.m1[b * d + bb], row, acc);
+    }
+    const double z = rho[e] * sqrt(1.0 / (rho[e] * kinv[e]));
+    atomicAdd(out_p + g[face_node(axis, side, d, a, b)], cs * (((axis == 0 ? area_x : area_y) / z) * acc));
+  }
+}
+
+// Free-surface lumped mass (:268-276): lump_p[top face] += (1/(rho g)) (area l1_b l1_a)
+__global__ void mix_surface_lump_kernel(const __grid_constant__ FaceTabs ft, double* __restrict__ lump_p,
+                                        const int* __restrict__ gids, int64_t gs,
+                                        const double* __restrict__ rho, int nx, int ny, int nz, int d,
+                                        double area, double g) {
+  const int64_t nf = (int64_t)nx * ny;
+  const int d2 = d * d;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nf * d2;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = t / d2;
+    const int node = (int)(t - f * d2), a = node % d, b = node / d;
+    const int64_t e = f + nf * (nz - 1);
+    atomicAdd(lump_p + gids[e * gs + face_node(2, 1, d, a, b)],
+              (1.0 / (rho[e] * g)) * (area * (ft.l1[b] * ft.l1[a])));
+  }
+}
+
+// bottom_face_load (:441-460): load[bottom face] += area * (kron(m1, m1) vals_f)
+__global__ void mix_bottom_load_kernel(const __grid_constant__ FaceTabs ft, double* __restrict__ load,
+                                       const double* __restrict__ vals, const int* __restrict__ gids,
+                                       int64_t gs, int nx, int ny, int d, double area) {
+  const int64_t nf = (int64_t)nx * ny;
+  const int d2 = d * d;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nf * d2;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = t / d2;
+    const int node = (int)(t - f * d2), a = node % d, b = node / d;
+    const double* v = vals + f * d2;
+    double acc = 0.0;
+    for (int bb = 0; bb < d; ++bb) {
+      double row = 0.0;
+      for (int aa = 0; aa < d; ++aa) row = fma(ft.m1[a * d + aa], v[aa + d * bb], row);
+      acc = fma(ft.m1[b * d + bb], row, acc);
+    }
+    atomicAdd(load + gids[f * gs + face_node(2, 0, d, a, b)], area * acc);
   }
 }
 
@@ -186,6 +281,10 @@ struct fk_mix {
   double* zbuf = nullptr;    // fused-normal intermediate (ndof_p)
   double* rk = nullptr;      // rk4 work: 4 stage vectors, stage state, residual, state
   cudaEvent_t ev[4] = {};
+  // boundary terms
+  FaceTabs face{};
+  double* rho_d = nullptr;   // per-element density / inverse bulk modulus (device)
+  double* kinv_d = nullptr;
 };
 
 namespace {
@@ -217,8 +316,18 @@ int mix_apply_dev(fk_mix* m, const double* u, const double* p, double* out_u, do
                   cudaStream_t s) {
   FK_CUDA(cudaMemsetAsync(out_p, 0, sizeof(double) * m->ndof_p, s));
   const double cs = m->desc.coupling_scale;
-  return mix_launch_mode(m, u, p, out_u, out_p, m->desc.matrix_free ? MIX_BOTH_MF : MIX_BOTH, cs,
-                         -cs, s);
+  FK_TRY(mix_launch_mode(m, u, p, out_u, out_p, m->desc.matrix_free ? MIX_BOTH_MF : MIX_BOTH, cs,
+                         -cs, s));
+  if (m->desc.absorbing) {
+    const int nx = m->desc.nx, ny = m->desc.ny, nz = m->desc.nz, d = m->dp;
+    const int64_t work = 2 * ((int64_t)ny * nz + (int64_t)nx * nz) * d * d;
+    const double* jd = m->desc.jac_diag;  // h/2: area of an x face (h_y/2)(h_z/2)
+    mix_absorb_kernel<<<grid_for(work, 256, m->num_sms), 256, 0, s>>>(
+        m->face, out_p, p, m->gids, m->kern->gs, m->rho_d, m->kinv_d, nx, ny, nz, d, jd[1] * jd[2],
+        jd[0] * jd[2], cs);
+    FK_CUDA(cudaGetLastError());
+  }
+  return FK_OK;
 }
 
 }  // namespace
@@ -247,6 +356,8 @@ int fk_mix_create(fk_mix** out, const fk_mix_desc* d) {
       !fk::mirror_symmetric(d->Bu, nullptr, d->num_quad_1d, d->order_u + 1))
     return fk_fail(FK_EUNSUPPORTED, "the block operator kernels need mirror-symmetric basis tables "
                                     "(symmetric nodes and quadrature points)");
+  if (d->surface_gravity < 0.0 || !(d->surface_gravity == d->surface_gravity))
+    return fk_fail(FK_EINVAL, "surface gravity must be positive");
   fk_mix* m = new fk_mix();
   m->desc = *d;
   m->dp = d->order_p + 1;
@@ -326,10 +437,23 @@ int fk_mix_setup(fk_mix* m) {
     return x;  // (d, d, d) x fastest
   };
   std::vector<double> lu = lump_ref(m->Bu, m->du), lp = lump_ref(m->Bp, m->dp);
-  double *d_ref = nullptr, *d_rho = nullptr, *d_kinv = nullptr;
+  double* d_ref = nullptr;
   FK_CUDA(cudaMalloc(&d_ref, sizeof(double) * (du3 + dp3)));
-  FK_CUDA(cudaMalloc(&d_rho, sizeof(double) * m->nel));
-  FK_CUDA(cudaMalloc(&d_kinv, sizeof(double) * m->nel));
+  if (m->rho_d == nullptr) FK_CUDA(cudaMalloc(&m->rho_d, sizeof(double) * m->nel));
+  if (m->kinv_d == nullptr) FK_CUDA(cudaMalloc(&m->kinv_d, sizeof(double) * m->nel));
+  double* d_rho = m->rho_d;
+  double* d_kinv = m->kinv_d;
+  // face tables m1 = Bp^T W Bp, l1 = Bp^T w (_init_boundary_terms, operator.py:420-427)
+  for (int i = 0; i < m->dp; ++i) {
+    double l = 0.0;
+    for (int a2 = 0; a2 < q; ++a2) l += m->Bp[a2 * m->dp + i] * m->w[a2];
+    m->face.l1[i] = l;
+    for (int j = 0; j < m->dp; ++j) {
+      double s2 = 0.0;
+      for (int a2 = 0; a2 < q; ++a2) s2 += m->Bp[a2 * m->dp + i] * (m->w[a2] * m->Bp[a2 * m->dp + j]);
+      m->face.m1[i * m->dp + j] = s2;
+    }
+  }
   FK_CUDA(cudaMemcpyAsync(d_ref, lu.data(), sizeof(double) * du3, cudaMemcpyHostToDevice, s));
   FK_CUDA(cudaMemcpyAsync(d_ref + du3, lp.data(), sizeof(double) * dp3, cudaMemcpyHostToDevice, s));
   FK_CUDA(cudaMemcpyAsync(d_rho, m->rho.data(), sizeof(double) * m->nel, cudaMemcpyHostToDevice, s));
@@ -342,10 +466,15 @@ int fk_mix_setup(fk_mix* m) {
   mix_lump_p_kernel<<<grid_for(m->nel * dp3, 256, m->num_sms), 256, 0, s>>>(
       m->lump_p, m->gids, d_kinv, d_ref + du3, m->nel, dp3, k.gs);
   FK_CUDA(cudaGetLastError());
+  if (m->desc.surface_gravity > 0.0) {  // after the volume lump, as the reference
+    const int64_t work = (int64_t)m->desc.nx * m->desc.ny * m->dp * m->dp;
+    mix_surface_lump_kernel<<<grid_for(work, 256, m->num_sms), 256, 0, s>>>(
+        m->face, m->lump_p, m->gids, k.gs, d_rho, m->desc.nx, m->desc.ny, m->desc.nz, m->dp,
+        m->desc.jac_diag[0] * m->desc.jac_diag[1], m->desc.surface_gravity);
+    FK_CUDA(cudaGetLastError());
+  }
   FK_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_ref);
-  cudaFree(d_rho);
-  cudaFree(d_kinv);
   for (const void* f : {k.f_both, k.f_tau, k.f_vb})
     FK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem));
   FK_CUDA(cudaFuncSetAttribute(k.f_mf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem_mf));
@@ -406,7 +535,8 @@ int fk_mix_mass_inverse(fk_mix* m, const double* ru, const double* rp, double* u
   return FK_OK;
 }
 
-int fk_mix_rk4(fk_mix* m, double* u, double* p, double dt, int steps) {
+static int mix_rk4(fk_mix* m, double* u, double* p, double dt, int steps, const double* f0,
+                   const double* fh, const double* f1) {
   if (m == nullptr || u == nullptr || p == nullptr) return fk_fail(FK_EINVAL, "null argument");
   if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
   if (!(dt > 0.0)) return fk_fail(FK_EINVAL, "dt must be positive, got %g", dt);
@@ -422,23 +552,46 @@ int fk_mix_rk4(fk_mix* m, double* u, double* p, double dt, int steps) {
   cudaStream_t s = m->stream;
   const int gb = grid_for(n, 256, m->num_sms);
   // one stage: r = A x, then the fused k / acc / next-state update
-  auto stage = [&](const double* x, double c_acc, double c_next, int first, double* acc_out) -> int {
+  auto stage = [&](const double* x, double c_acc, double c_next, int first, double* acc_out,
+                   const double* f) -> int {
     FK_TRY(mix_apply_dev(m, x, x + nu, res, res + nu, s));
     mix_rk4_stage_kernel<<<gb, 256, 0, s>>>(res, m->lump_u, nu, m->nel * du3, m->lump_p, y, acc,
-                                            acc_out, ytmp, c_acc, c_next, first, n);
+                                            acc_out, ytmp, c_acc, c_next, first, n, f);
     FK_CUDA(cudaGetLastError());
     return FK_OK;
   };
   FK_CUDA(cudaMemcpyAsync(y, u, sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
   FK_CUDA(cudaMemcpyAsync(y + nu, p, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice, s));
   for (int st = 0; st < steps; ++st) {
-    FK_TRY(stage(y, dt / 6, dt / 2, 1, acc));     // k1
-    FK_TRY(stage(ytmp, dt / 3, dt / 2, 0, acc));  // k2
-    FK_TRY(stage(ytmp, dt / 3, dt, 0, acc));      // k3
-    FK_TRY(stage(ytmp, dt / 6, 0.0, 0, y));       // k4: y = acc + dt/6 k4
+    FK_TRY(stage(y, dt / 6, dt / 2, 1, acc, f0));     // k1 = rhs(t)
+    FK_TRY(stage(ytmp, dt / 3, dt / 2, 0, acc, fh));  // k2 = rhs(t + dt/2)
+    FK_TRY(stage(ytmp, dt / 3, dt, 0, acc, fh));      // k3 = rhs(t + dt/2)
+    FK_TRY(stage(ytmp, dt / 6, 0.0, 0, y, f1));       // k4 = rhs(t + dt): y = acc + dt/6 k4
   }
   FK_CUDA(cudaMemcpyAsync(u, y, sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
   FK_CUDA(cudaMemcpyAsync(p, y + nu, sizeof(double) * m->ndof_p, cudaMemcpyDeviceToDevice, s));
+  return FK_OK;
+}
+
+int fk_mix_rk4(fk_mix* m, double* u, double* p, double dt, int steps) {
+  return mix_rk4(m, u, p, dt, steps, nullptr, nullptr, nullptr);
+}
+
+int fk_mix_rk4_forced(fk_mix* m, double* u, double* p, double dt, const double* f0,
+                      const double* fh, const double* f1) {
+  return mix_rk4(m, u, p, dt, 1, f0, fh, f1);
+}
+
+int fk_mix_bottom_load(fk_mix* m, const double* vals, double* load) {
+  if (m == nullptr || vals == nullptr || load == nullptr) return fk_fail(FK_EINVAL, "null argument");
+  if (!m->is_setup) return fk_fail(FK_EINVAL, "fk_mix_setup has not been called");
+  FkDeviceGuard g(m->device);
+  FK_CUDA(cudaMemsetAsync(load, 0, sizeof(double) * m->ndof_p, m->stream));
+  const int64_t work = (int64_t)m->desc.nx * m->desc.ny * m->dp * m->dp;
+  mix_bottom_load_kernel<<<grid_for(work, 256, m->num_sms), 256, 0, m->stream>>>(
+      m->face, load, vals, m->gids, m->kern->gs, m->desc.nx, m->desc.ny, m->dp,
+      m->desc.jac_diag[0] * m->desc.jac_diag[1]);
+  FK_CUDA(cudaGetLastError());
   return FK_OK;
 }
 
@@ -509,6 +662,8 @@ int fk_mix_destroy(fk_mix* m) {
   cudaFree(m->rk);
   for (auto& e : m->ev)
     if (e) cudaEventDestroy(e);
+  cudaFree(m->rho_d);
+  cudaFree(m->kinv_d);
   delete m;
   return FK_OK;
 }

@@ -60,8 +60,13 @@ class MixedOperator:
 
     Supported: order_u = order_p - 1, num_quad_1d = order_p + 1, order_p = 2..8
     (the reference default 4/3/5), scalar or per-element rho / bulk modulus,
-    coupling_scale.  Not supported (raise): absorbing faces, surface gravity
-    (operator.py:400-440).  strategy MF / FusedMF recomputes dmat in the kernel.
+    coupling_scale, absorbing lateral faces (applied on the device inside
+    every apply and RK4 stage, :357-358, 432-439), free-surface gravity
+    (lumped-mass term, :268-276; ``surface_height``), ``bottom_face_load``
+    (:441-460) and forced RK4 (:506-531).  strategy MF / FusedMF recomputes
+    dmat in the kernel.  Counters follow the reference: one operator_apply
+    and the contraction flops per apply, d_reads 2x / 1x / 0 of the stored
+    dmat for PA / FusedPA / MF (``_dfactors``, :280-286).
     """
 
     def __init__(self, mesh, order_p: int = 4, order_u: int = 3, num_quad_1d: int = 5,
@@ -71,8 +76,10 @@ class MixedOperator:
                  stream=None):
         if strategy not in STRATEGIES:
             raise ValueError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
-        if absorbing or surface_gravity is not None:
-            raise NotImplementedError("absorbing faces / surface gravity are not on the B200 path")
+        if surface_gravity is not None and not float(surface_gravity) > 0:
+            raise ValueError("surface gravity must be positive")
+        self.absorbing = bool(absorbing)
+        self.surface_gravity = None if surface_gravity is None else float(surface_gravity)
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("MixedOperator needs a CUDA device (there is no CPU fallback)")
@@ -112,6 +119,8 @@ class MixedOperator:
         desc.rho_scalar = desc.bulk_scalar = 1.0
         desc.coupling_scale = self.coupling_scale
         desc.matrix_free = 1 if strategy in ("MF", "FusedMF") else 0
+        desc.absorbing = 1 if self.absorbing else 0
+        desc.surface_gravity = 0.0 if self.surface_gravity is None else self.surface_gravity
         desc.device = self.device.index
         desc.stream = ctypes.c_void_p(self._stream.cuda_stream)
         h = ctypes.c_void_p()
@@ -126,6 +135,13 @@ class MixedOperator:
         self.num_dofs_u_local = (self.order_u + 1) ** 3
         self.num_dofs = int(info.ndof_u) + self.num_p
         self._zero_u = None
+        # reference counter semantics (counters.py; tensor.py:204-205 counts
+        # 2 d q e1 e2 per contraction; _dfactors :280-286 counts dmat reads)
+        chain = lambda n, m: 2 * n * m * (n * n + n * m + m * m)  # noqa: E731
+        dp, du, q = self.order_p + 1, self.order_u + 1, self.num_quad_1d
+        self.flops_per_apply = 6 * self.num_elements * (chain(dp, q) + chain(du, q))
+        per = 9 * q ** 3 * self.num_elements
+        self.d_reads_per_apply = {"PA": 2 * per, "FusedPA": per}.get(strategy, 0)
 
     # -- lifecycle ------------------------------------------------------------
 
@@ -176,7 +192,7 @@ class MixedOperator:
     def apply(self, state, out: State | None = None) -> State:
         """Residual of the coupling operator acting on [u, p] (operator.py:331-362)."""
         self._check(state)
-        self.counters.operator_applies += 1
+        self._count(1)
         host = isinstance(state.u, np.ndarray)
         u, p = self._dev(state.u), self._dev(state.p)
         torch = _torch()
@@ -190,6 +206,13 @@ class MixedOperator:
 
     __call__ = apply
 
+    def _count(self, applies: int, normal: int = 0) -> None:
+        """applies: BlockOperator.apply calls; normal: apply_fused_normal calls
+        (which the reference does not count as operator applies)."""
+        self.counters.operator_applies += applies
+        self.counters.flops += (applies + normal) * self.flops_per_apply
+        self.counters.d_reads += (applies + normal) * self.d_reads_per_apply
+
     def apply_fused_normal(self, x_u):
         """Velocity -> assembled pressure -> velocity (operator.py:364-387)."""
         host = isinstance(x_u, np.ndarray)
@@ -197,6 +220,7 @@ class MixedOperator:
             raise ValueError(f"velocity dimensions {tuple(x_u.shape)} do not match {self.u_shape}")
         u = self._dev(x_u)
         out = _torch().empty_like(u)
+        self._count(0, 1)
         _lib.check(self._lib.fk_mix_fused_normal(self._h, u.data_ptr(), out.data_ptr()))
         return out.cpu().numpy() if host else out
 
@@ -234,7 +258,7 @@ class MixedOperator:
             raise ValueError(f"dt must be positive, got {dt}")
         host = isinstance(state.u, np.ndarray)
         u, p = self._dev(state.u).clone(), self._dev(state.p).clone()
-        self.counters.operator_applies += 4 * int(steps)
+        self._count(4 * int(steps))
         _lib.check(self._lib.fk_mix_rk4(self._h, u.data_ptr(), p.data_ptr(), float(dt), int(steps)))
         torch = _torch()
         if not (bool(torch.isfinite(u).all()) and bool(torch.isfinite(p).all())):
@@ -261,16 +285,82 @@ class MixedOperator:
     def gather_ids(self) -> np.ndarray:
         return h1_gather_ids(self.mesh.nx, self.mesh.ny, self.mesh.nz, self.order_p + 1)
 
+    # -- boundary terms (operator.py:400-470) ------------------------------------
+
+    def _face_ids(self, ez: int, side: int) -> np.ndarray:
+        """(nx*ny, dp^2) global pressure ids of the z-faces of element layer
+        ``ez`` (side 0 low, 1 high), faces x-fastest, face nodes first
+        in-plane index fastest (_face_local_indices, :201-210)."""
+        d, nx, ny = self.order_p + 1, self.mesh.nx, self.mesh.ny
+        npx, npy = nx * (d - 1) + 1, ny * (d - 1) + 1
+        ey, ex = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+        b, a = np.meshgrid(np.arange(d), np.arange(d), indexing="ij")
+        gi = ex.reshape(-1, 1) * (d - 1) + a.reshape(1, -1)
+        gj = ey.reshape(-1, 1) * (d - 1) + b.reshape(1, -1)
+        gk = ez * (d - 1) + (d - 1 if side else 0)
+        return gi + npx * (gj + npy * gk)
+
+    def bottom_face_load(self, profile) -> np.ndarray:
+        """Assembled load of a normal-velocity profile(x, y) on the bottom
+        face (operator.py:441-460): the profile is evaluated per bottom face
+        at its node positions (host callable), the face mass pairing and the
+        assembly run on the device.  Returns a NumPy vector of num_p."""
+        torch = _torch()
+        d, nx, ny = self.order_p + 1, self.mesh.nx, self.mesh.ny
+        nodes = np.asarray(self.basis_p.nodes, dtype=np.float64)
+        h = 2.0 * np.asarray(self.mesh.jacobian_diag, dtype=np.float64)
+        vals = np.empty((nx * ny, d * d))
+        for f in range(nx * ny):
+            ex, ey = f % nx, f // nx
+            xs = ex * h[0] + (nodes + 1.0) * 0.5 * h[0]
+            ys = ey * h[1] + (nodes + 1.0) * 0.5 * h[1]
+            gx, gy = np.meshgrid(xs, ys, indexing="ij")
+            vals[f] = np.asarray(profile(gx.ravel(order="F"), gy.ravel(order="F")), dtype=np.float64)
+        v = torch.as_tensor(vals, device=self.device)
+        load = torch.empty(self.num_p, dtype=torch.float64, device=self.device)
+        _lib.check(self._lib.fk_mix_bottom_load(self._h, v.data_ptr(), load.data_ptr()))
+        return load.cpu().numpy()
+
+    def surface_height(self, state) -> np.ndarray:
+        """Free-surface elevation p / (rho g) at the surface-face nodes
+        (operator.py:462-470), faces x-fastest."""
+        if self.surface_gravity is None:
+            raise ValueError("operator was built without surface gravity")
+        torch = _torch()
+        ids = self._face_ids(self.mesh.nz - 1, 1)
+        top = np.arange(self.mesh.nx * self.mesh.ny) + self.mesh.nx * self.mesh.ny * (self.mesh.nz - 1)
+        p = self._dev(state.p)
+        vals = p[torch.as_tensor(ids.ravel(), device=self.device)].reshape(ids.shape)
+        rho = torch.as_tensor(self._rho[top], device=self.device)
+        return (vals / (rho[:, None] * self.surface_gravity)).reshape(-1).cpu().numpy()
+
+    def rk4_forced(self, state, dt: float, f0, fh, f1) -> State:
+        """One RK4 step with forcing values at t, t + dt/2, t + dt (States)."""
+        self._check(state)
+        torch = _torch()
+        host = isinstance(state.u, np.ndarray)
+        u, p = self._dev(state.u).clone(), self._dev(state.p).clone()
+        packed = []
+        for f in (f0, fh, f1):
+            packed.append(torch.cat([self._dev(f.u).reshape(-1), self._dev(f.p).reshape(-1)]))
+        self._count(4)
+        _lib.check(self._lib.fk_mix_rk4_forced(self._h, u.data_ptr(), p.data_ptr(), float(dt),
+                                               *(t.data_ptr() for t in packed)))
+        if not (bool(torch.isfinite(u).all()) and bool(torch.isfinite(p).all())):
+            raise DivergenceError("non-finite state after the forced step")
+        return State(u.cpu().numpy(), p.cpu().numpy()) if host else State(u, p)
+
 
 def rk4_step(state, dt: float, op: MixedOperator, forcing=None, t: float = 0.0,
              step_index: int = 0) -> State:
-    """Classical RK4 step (operator.py:506-531) on the device; forcing is not
-    supported on the B200 path."""
-    if forcing is not None:
-        raise NotImplementedError("forcing is not supported by the device RK4 driver")
+    """Classical RK4 step of [u, p]' = Minv(-A[u, p] + f) (operator.py:506-531)
+    on the device.  ``forcing(time) -> State`` is evaluated at t, t + dt/2
+    and t + dt (the reference calls it at t + dt/2 for both middle stages)."""
     if dt <= 0:
         raise ValueError(f"dt must be positive, got {dt}")
     try:
+        if forcing is not None:
+            return op.rk4_forced(state, dt, forcing(t), forcing(t + dt / 2), forcing(t + dt))
         return op.rk4(state, dt, 1)
     except DivergenceError as ex:
         raise DivergenceError(f"non-finite state after step {step_index}") from ex

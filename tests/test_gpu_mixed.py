@@ -137,8 +137,7 @@ def test_device_state_and_errors():
         MixedOperator(build_mesh(2, 2, 2), strategy="scalar")
     with pytest.raises(NotImplementedError):
         MixedOperator(build_mesh(2, 2, 2), order_u=2)
-    with pytest.raises(NotImplementedError):
-        MixedOperator(build_mesh(2, 2, 2), absorbing=True)
+    assert MixedOperator(build_mesh(2, 2, 2), absorbing=True).absorbing  # now on the device path
 
 
 def test_linear_pressure_gives_mass_weighted_unit_field():
