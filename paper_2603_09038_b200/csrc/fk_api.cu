@@ -316,7 +316,8 @@ static int preload_kernels(const fk_op* op) {
                       reinterpret_cast<const void*>(&fk::cg_finish_kernel),
                       reinterpret_cast<const void*>(&fk::cg_step_kernel),
                       reinterpret_cast<const void*>(&fk::qf_sum_kernel),
-                      reinterpret_cast<const void*>(&fk::recip_kernel)};
+                      reinterpret_cast<const void*>(&fk::recip_kernel),
+                      reinterpret_cast<const void*>(&fk::diag_box_kernel)};
   cudaFuncAttributes a;
   for (const void* k : ks) FK_CUDA(cudaFuncGetAttributes(&a, k));
   for (const auto& k : registry()) {
@@ -564,6 +565,7 @@ int fk_op_destroy(fk_op* op) {
   cudaFree(op->counter);
   cudaFree(op->hist);
   cudaFree(op->qf_part);
+  cudaFree(op->diag_tab);
   cudaFree(op->halo);
   if (op->comm_stream) cudaStreamDestroy(op->comm_stream);
   if (op->ev_bnd) cudaEventDestroy(op->ev_bnd);
@@ -740,6 +742,58 @@ int fk_op_diagonal(fk_op* op, double* diag) {
   if (op == nullptr || diag == nullptr) return fail(FK_EINVAL, "null argument");
   if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
   DeviceGuard g(op->device);
+  if (op->host_gids.empty()) {
+    // structured box: separable closed form, one pass (fk_setup.cuh diag_box_kernel)
+    if (op->diag_tab == nullptr) {
+      const int64_t np3 = op->npx + op->npy + op->npz_local;
+      std::vector<double> h(2 * np3, 0.0);
+      const int d = op->d, q = op->q, p = op->p;
+      double fb[9] = {}, fg[9] = {};
+      for (int i = 0; i < d; ++i)
+        for (int a = 0; a < q; ++a) {
+          fb[i] += op->w[a] * (op->B[a * d + i] * op->B[a * d + i]);
+          fg[i] += op->w[a] * (op->G[a * d + i] * op->G[a * d + i]);
+        }
+      // assembled 1D factor over n elements: node g takes f(g % p) from the
+      // element on its left (local index p when g % p == 0) and on its right
+      auto assemble = [&](double* out, int64_t npn, const double* f) {
+        for (int64_t g = 0; g < npn; ++g) {
+          double v = 0.0;
+          if (g % p != 0) v = f[g % p];
+          else {
+            if (g > 0) v += f[p];
+            if (g < npn - 1) v += f[0];
+          }
+          out[g] = v;
+        }
+      };
+      double* t = h.data();
+      assemble(t, op->npx, fb);
+      assemble(t + op->npx, op->npx, fg);
+      t += 2 * op->npx;
+      assemble(t, op->npy, fb);
+      assemble(t + op->npy, op->npy, fg);
+      t += 2 * op->npy;
+      assemble(t, op->npz_local, fb);
+      assemble(t + op->npz_local, op->npz_local, fg);
+      FK_CUDA(cudaMalloc(&op->diag_tab, sizeof(double) * h.size()));
+      FK_CUDA(cudaMemcpyAsync(op->diag_tab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
+                              op->stream));
+      FK_CUDA(cudaStreamSynchronize(op->stream));
+    }
+    const double dj = op->desc.jac_det;
+    fk::diag_box_kernel<<<grid_for(op->ndof, 256, op->num_sms), 256, 0, op->stream>>>(
+        diag, op->diag_tab, op->npx, op->npy, op->npz_local, op->nc, dj * (op->jinv[0] * op->jinv[0]),
+        dj * (op->jinv[1] * op->jinv[1]), dj * (op->jinv[2] * op->jinv[2]), dj);
+    FK_CUDA(cudaGetLastError());
+    if (op->comm) FK_TRY(fk::exchange_interface(op, diag, op->stream));
+    if (op->desc.dirichlet && op->n_ess > 0) {
+      fk::ess_set_kernel<<<grid_for(op->n_ess, 256, op->num_sms), 256, 0, op->stream>>>(
+          diag, op->ess, op->n_ess, 1.0);
+      FK_CUDA(cudaGetLastError());
+    }
+    return FK_OK;
+  }
   FK_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * op->ndof, op->stream));
   const fk::KernelEntry* k = fk::find_kernel(op->nc, op->d, op->q, FK_VARIANT_DFMA);
   if (k == nullptr || k->diag == nullptr) return fail(FK_EUNSUPPORTED, "no diagonal kernel");

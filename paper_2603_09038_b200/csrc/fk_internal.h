@@ -186,6 +186,7 @@ struct fk_op {
   // CG: p.Ap as the fused kernel's quadratic form (per-CTA partials of up to 8
   // launches per apply: the colour launches / the overlapped layer ranges)
   double* qf_part = nullptr;
+  double* diag_tab = nullptr;  // assembled 1D factors of the closed-form box diagonal
   bool qf_on = false;
   int qf_seg = 0;
   // multi-rank

@@ -87,3 +87,19 @@ def test_mixed_rejects_unsymmetric_tables(monkeypatch):
     monkeypatch.setattr(mixed.Basis1D, "nodal", staticmethod(skewed))
     with pytest.raises(NotImplementedError, match="symmetric"):
         MixedOperator(fem.build_mesh(2, 2, 2), 4, 3, 5)
+
+
+@pytest.mark.parametrize("kind,p", [("diffusion", 3), ("diffusion", 6), ("mass", 4)])
+def test_diagonal_closed_form_and_general_kernel_agree(kind, p):
+    """The box diagonal is one separable closed-form pass (fk_setup.cuh
+    diag_box_kernel); a caller-supplied gather map takes the general
+    element-wise kernel.  Both match the oracle's assembled diagonal."""
+    n = (4, 3, 5)
+    mesh = fem.build_mesh(*n, extents=(2.0, 1.0, 0.5))
+    P = bp.Problem(kind, *n, p, extents=(2.0, 1.0, 0.5))
+    ref = P.diagonal()
+    box = PAOperator(mesh, p, kind=kind).diagonal().cpu().numpy()
+    gen = PAOperator(mesh, p, kind=kind, restriction=fem.h1_restriction(mesh, p + 1)).diagonal().cpu().numpy()
+    scale = np.abs(ref).max()
+    assert np.abs(box - ref).max() <= 1e-13 * scale
+    assert np.abs(gen - ref).max() <= 1e-13 * scale
