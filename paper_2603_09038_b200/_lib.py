@@ -146,7 +146,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    # FK_LIB_PATH: an alternative build of the same library (A/B tooling,
+    # tools/build_variant.py); never set on the product path
+    path = path or os.environ.get("FK_LIB_PATH") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build it with `python -m paper_2603_09038_b200.build` "

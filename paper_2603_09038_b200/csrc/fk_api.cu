@@ -193,6 +193,9 @@ int select_kernel(fk_op* op, int variant) {
     DeviceGuard g(op->device);
     FK_CUDA(cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)k->smem));
+    if (k->func_qf)
+      FK_CUDA(cudaFuncSetAttribute(k->func_qf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)k->smem));
     int occ = 0;
     FK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->func, k->T, k->smem));
     if (occ < 1) return fail(FK_EUNSUPPORTED, "fused kernel does not fit on an SM (smem %zu)", k->smem);
@@ -222,7 +225,7 @@ int launch_all(fk_op* op, const double* x, double* y, cudaStream_t s) {
   }
   fk::OpView v = view(op);
   if (op->qf_on) v.qf = op->qf_part + (size_t)op->qf_seg++ * op->max_blocks;
-  op->kern->launch(v, x, y, op->blocks, s);
+  (op->qf_on ? op->kern->launch_qf : op->kern->launch)(v, x, y, op->blocks, s);
   FK_CUDA(cudaGetLastError());
   return FK_OK;
 }
@@ -245,7 +248,7 @@ int launch_range(fk_op* op, const double* x, double* y, int64_t e0, int64_t ne, 
   const int64_t nb = (ne + op->kern->E - 1) / op->kern->E;
   const int blocks =
       (int)std::max<int64_t>(1, op->kern->persist ? std::min<int64_t>(nb, op->max_blocks) : nb);
-  op->kern->launch(v, x, y, blocks, s);
+  (op->qf_on ? op->kern->launch_qf : op->kern->launch)(v, x, y, blocks, s);
   FK_CUDA(cudaGetLastError());
   return FK_OK;
 }
@@ -323,6 +326,7 @@ static int preload_kernels(const fk_op* op) {
   for (const auto& k : registry()) {
     if (k.nc != op->nc || k.d != op->d || k.q != op->q) continue;
     FK_CUDA(cudaFuncGetAttributes(&a, k.func));
+    if (k.func_qf) FK_CUDA(cudaFuncGetAttributes(&a, k.func_qf));
     if (k.diag_func) FK_CUDA(cudaFuncGetAttributes(&a, k.diag_func));
   }
   return fk::preload_comm_kernels();
@@ -861,7 +865,7 @@ static int cg_iteration(fk_op* op, double* x, cudaStream_t s) {
   double* dinv = Ap + n;
   int* iscal = reinterpret_cast<int*>(op->scal + 16);
   const int rb = red_blocks(op);
-  const bool qf = op->kern->qf && op->qf_part != nullptr;
+  const bool qf = op->kern->launch_qf != nullptr && op->qf_part != nullptr;
   if (qf) {
     FK_CUDA(cudaMemsetAsync(op->qf_part, 0, sizeof(double) * 8 * op->max_blocks, s));
     op->qf_on = true;

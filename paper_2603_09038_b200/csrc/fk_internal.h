@@ -20,7 +20,8 @@ struct KernelEntry {
   int E = 0, T = 0;
   bool persist = true;  // persistent grid (batches strided over CTAs) or one batch per CTA
   bool structured = false;  // ids from the closed-form box restriction (no user gather map)
-  bool qf = false;          // can accumulate the element quadratic form (OpView::qf)
+  LaunchFn launch_qf = nullptr;  // twin with the element quadratic form (OpView::qf), CG only
+  const void* func_qf = nullptr;
   size_t smem = 0;
   const void* func = nullptr;
   const void* diag_func = nullptr;  // the assembled-diagonal kernel of this (d, q, nc)

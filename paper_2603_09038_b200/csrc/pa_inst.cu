@@ -45,13 +45,13 @@ StructIds struct_ids(const OpView& v) {
 }
 
 template <int D, int Q, int NC, class Body, bool PERSIST, bool DG, bool MF = false, int GM = 0,
-          bool SX = false, bool XP = false>
+          bool SX = false, bool XP = false, bool QF = false>
 void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
   typename Body::Tab tb;
   Body::fill(tb, v.B, v.G);
   if constexpr (MF) Body::fill_mf(tb, v.w, v.detj, v.jinv);
   const StructIds sid = struct_ids(v);
-  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>
+  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, QF>
       <<<blocks, Body::T, PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES, s>>>(
           tb, x, y, v.gids, v.pa, v.ebits, v.nel, sid);
 }
@@ -64,9 +64,23 @@ void launch_diag(const OpView& v, double* diag, int64_t nel, int blocks, cudaStr
   diagonal_kernel<D, Q, NC><<<blocks, 128, 0, s>>>(tb, diag, v.gids, v.pa, nel);
 }
 
-template <int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false, bool MF = false,
-          int GM = 0, bool SX = false, bool XP = false>
-KernelEntry entry(int variant, int cfg) {
+// Geometries that CG may select (fk_api.cu: kAutoCfg3 / kAutoCfgMF3 for q = p+2
+// and the array-map tables of the deterministic mode) get a twin instance with
+// the element quadratic form compiled in (QF, CG's p.Ap); every other launch
+// runs the kernel without it (measured 1-3% faster than a runtime switch).
+constexpr bool qf_cfg(int variant, int cfg) {
+  return variant == FK_VARIANT_EO
+             ? (cfg == 1 || cfg == 2 || cfg == 11 || cfg == 14 || cfg == 18 || cfg == 23 ||
+                cfg == 25 || cfg == 35)
+             : variant == FK_VARIANT_MF ? (cfg == 2 || cfg == 5 || cfg == 6 || cfg == 7 || cfg == 8 ||
+                                           cfg == 10)
+                                        : false;
+}
+
+template <int V, int CFG, int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false,
+          bool MF = false, int GM = 0, bool SX = false, bool XP = false>
+KernelEntry entry() {
+  constexpr int variant = V, cfg = CFG;
   KernelEntry k;
   k.nc = NC;
   k.d = D;
@@ -77,7 +91,11 @@ KernelEntry entry(int variant, int cfg) {
   k.T = Body::T;
   k.persist = PERSIST;
   k.structured = GM == 1;
-  k.qf = HasQf<Body>::value && PERSIST;
+  if constexpr (NC == 3 && Q == D + 1 && PERSIST && HasQf<Body>::value && qf_cfg(V, CFG))
+  {
+    k.launch_qf = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, true>;
+    k.func_qf = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, true>);
+  }
   k.smem = PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES;
   k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>);
   k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>;
@@ -92,20 +110,20 @@ using TunedEo =
 
 // nine tuned even-odd geometries from cfg c0: (E2, E1) x (smem D, D via L2) x
 // (W over T1, W over T2), then E0 in place
-template <int D, int Q, int NC, bool PP>
-void add_tuned_eo(std::vector<KernelEntry>& out, int c0) {
+template <int D, int Q, int NC, bool PP, int C0>
+void add_tuned_eo(std::vector<KernelEntry>& out) {
   constexpr int E0 = base_E(Q);
   constexpr int E1 = E0 / 2 > 0 ? E0 / 2 : 1;
   constexpr int E2 = E0 / 4 > 0 ? E0 / 4 : 1;
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, PP>, true>(FK_VARIANT_EO, c0 + 0));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, PP>, true>(FK_VARIANT_EO, c0 + 1));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, PP>, true, true>(FK_VARIANT_EO, c0 + 2));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, PP>, true, true>(FK_VARIANT_EO, c0 + 3));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, PP>, true>(FK_VARIANT_EO, c0 + 4));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, true, PP>, true>(FK_VARIANT_EO, c0 + 5));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, PP>, true, true>(FK_VARIANT_EO, c0 + 6));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, true, PP>, true, true>(FK_VARIANT_EO, c0 + 7));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, PP>, true>(FK_VARIANT_EO, c0 + 8));
+  out.push_back(entry<FK_VARIANT_EO, C0 + 0, D, Q, NC, TunedEo<D, Q, NC, E2, false, PP>, true>());
+  out.push_back(entry<FK_VARIANT_EO, C0 + 1, D, Q, NC, TunedEo<D, Q, NC, E1, false, PP>, true>());
+  out.push_back(entry<FK_VARIANT_EO, C0 + 2, D, Q, NC, TunedEo<D, Q, NC, E2, false, PP>, true, true>());
+  out.push_back(entry<FK_VARIANT_EO, C0 + 3, D, Q, NC, TunedEo<D, Q, NC, E1, false, PP>, true, true>());
+  out.push_back(entry<FK_VARIANT_EO, C0 + 4, D, Q, NC, TunedEo<D, Q, NC, E2, true, PP>, true>());
+  out.push_back(entry<FK_VARIANT_EO, C0 + 5, D, Q, NC, TunedEo<D, Q, NC, E1, true, PP>, true>());
+  out.push_back(entry<FK_VARIANT_EO, C0 + 6, D, Q, NC, TunedEo<D, Q, NC, E2, true, PP>, true, true>());
+  out.push_back(entry<FK_VARIANT_EO, C0 + 7, D, Q, NC, TunedEo<D, Q, NC, E1, true, PP>, true, true>());
+  out.push_back(entry<FK_VARIANT_EO, C0 + 8, D, Q, NC, TunedEo<D, Q, NC, E0, true, PP>, true>());
 }
 
 // Compiled launch geometries (cfg index per variant), measured per order in
@@ -118,48 +136,48 @@ void add_all(std::vector<KernelEntry>& out) {
   using F1 = DfmaBody<D, Q, NC, E1, round32(E1 * Q * Q), 1>;
   using F2 = DfmaBody<D, Q, NC, E2, round32(E2 * Q * Q), 1>;
   using F1x2 = DfmaBody<D, Q, NC, E1, round32((E1 * Q * Q + 1) / 2), 2>;
-  out.push_back(entry<D, Q, NC, F2, true>(FK_VARIANT_DFMA, 0));
-  out.push_back(entry<D, Q, NC, F1, true>(FK_VARIANT_DFMA, 1));
-  out.push_back(entry<D, Q, NC, F2, true, true>(FK_VARIANT_DFMA, 2));   // D via L2, not smem
-  out.push_back(entry<D, Q, NC, F1, true, true>(FK_VARIANT_DFMA, 3));
-  out.push_back(entry<D, Q, NC, F1x2, true>(FK_VARIANT_DFMA, 4));       // 2 lines per thread
-  out.push_back(entry<D, Q, NC, F2, false>(FK_VARIANT_DFMA, 5));        // one batch per CTA
-  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true>(FK_VARIANT_DMMA, 0));
-  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E0, 256>, true>(FK_VARIANT_DMMA, 1));
-  out.push_back(entry<D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true, true>(FK_VARIANT_DMMA, 2));
+  out.push_back(entry<FK_VARIANT_DFMA, 0, D, Q, NC, F2, true>());
+  out.push_back(entry<FK_VARIANT_DFMA, 1, D, Q, NC, F1, true>());
+  out.push_back(entry<FK_VARIANT_DFMA, 2, D, Q, NC, F2, true, true>());   // D via L2, not smem
+  out.push_back(entry<FK_VARIANT_DFMA, 3, D, Q, NC, F1, true, true>());
+  out.push_back(entry<FK_VARIANT_DFMA, 4, D, Q, NC, F1x2, true>());       // 2 lines per thread
+  out.push_back(entry<FK_VARIANT_DFMA, 5, D, Q, NC, F2, false>());        // one batch per CTA
+  out.push_back(entry<FK_VARIANT_DMMA, 0, D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true>());
+  out.push_back(entry<FK_VARIANT_DMMA, 1, D, Q, NC, DmmaBody<D, Q, NC, E0, 256>, true>());
+  out.push_back(entry<FK_VARIANT_DMMA, 2, D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true, true>());
   using F0 = DfmaBody<D, Q, NC, E0, round32(E0 * Q * Q), 1>;
-  out.push_back(entry<D, Q, NC, F0, true>(FK_VARIANT_DFMA, 6));
+  out.push_back(entry<FK_VARIANT_DFMA, 6, D, Q, NC, F0, true>());
   // even-odd bodies.  cfg 0: the line layout of the first EO kernels (reference
   // point); cfgs 1-9: smem layouts searched by tools/smem_strides.py
   // (pa_eo_layouts.cuh) with ping-pong tables; cfgs 10-18: the same with a
   // static table copy (see DfmaEoBody PP).
   using O2 = DfmaEoBody<D, Q, NC, E2, round32(E2 * Q * Q), EoLayDefault<D, Q, NC, false>>;
-  out.push_back(entry<D, Q, NC, O2, true>(FK_VARIANT_EO, 0));
-  add_tuned_eo<D, Q, NC, true>(out, 1);
-  add_tuned_eo<D, Q, NC, false>(out, 10);
+  out.push_back(entry<FK_VARIANT_EO, 0, D, Q, NC, O2, true>());
+  add_tuned_eo<D, Q, NC, true, 1>(out);
+  add_tuned_eo<D, Q, NC, false, 10>(out);
   // closed-form restriction (no id traffic, 1 int per element per slot) with a
   // single X buffer: less smem per CTA -> more CTAs per SM
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, true>(FK_VARIANT_EO, 19));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, true>, true, false, false, 1, true>(FK_VARIANT_EO, 20));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, false>(FK_VARIANT_EO, 21));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, false>, true, false, false, 1, true>(FK_VARIANT_EO, 22));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, false>, true, false, false, 1, true>(FK_VARIANT_EO, 23));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true>(FK_VARIANT_EO, 24));
+  out.push_back(entry<FK_VARIANT_EO, 19, D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, true>());
+  out.push_back(entry<FK_VARIANT_EO, 20, D, Q, NC, TunedEo<D, Q, NC, E2, false, true>, true, false, false, 1, true>());
+  out.push_back(entry<FK_VARIANT_EO, 21, D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, false>());
+  out.push_back(entry<FK_VARIANT_EO, 22, D, Q, NC, TunedEo<D, Q, NC, E2, true, false>, true, false, false, 1, true>());
+  out.push_back(entry<FK_VARIANT_EO, 23, D, Q, NC, TunedEo<D, Q, NC, E1, false, false>, true, false, false, 1, true>());
+  out.push_back(entry<FK_VARIANT_EO, 24, D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true>());
   // cfgs 25-31: cfgs 2, 10, 14, 18, 19, 23, 24 with the gather slots precomputed (XP)
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, true>, true, false, false, 0, false, true>(FK_VARIANT_EO, 25));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, false>, true, false, false, 0, false, true>(FK_VARIANT_EO, 26));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, false>, true, false, false, 0, false, true>(FK_VARIANT_EO, 27));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 0, false, true>(FK_VARIANT_EO, 28));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, true, true>(FK_VARIANT_EO, 29));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, false, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 30));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 31));
+  out.push_back(entry<FK_VARIANT_EO, 25, D, Q, NC, TunedEo<D, Q, NC, E1, false, true>, true, false, false, 0, false, true>());
+  out.push_back(entry<FK_VARIANT_EO, 26, D, Q, NC, TunedEo<D, Q, NC, E2, false, false>, true, false, false, 0, false, true>());
+  out.push_back(entry<FK_VARIANT_EO, 27, D, Q, NC, TunedEo<D, Q, NC, E2, true, false>, true, false, false, 0, false, true>());
+  out.push_back(entry<FK_VARIANT_EO, 28, D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 0, false, true>());
+  out.push_back(entry<FK_VARIANT_EO, 29, D, Q, NC, TunedEo<D, Q, NC, E2, true, true>, true, false, false, 1, true, true>());
+  out.push_back(entry<FK_VARIANT_EO, 30, D, Q, NC, TunedEo<D, Q, NC, E1, false, false>, true, false, false, 1, true, true>());
+  out.push_back(entry<FK_VARIANT_EO, 31, D, Q, NC, TunedEo<D, Q, NC, E0, true, false>, true, false, false, 1, true, true>());
   // cfg 32: cfg 29 with separate table-row loads per component (SR off)
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 32));
+  out.push_back(entry<FK_VARIANT_EO, 32, D, Q, NC, TunedEo<D, Q, NC, E2, true, true, false>, true, false, false, 1, true, true>());
   // cfgs 33-35: more SR-off closed-form geometries (33: W over T1; 34: two X
   // buffers; 35: E1 elements per CTA, the BP3 p=4 default)
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, false, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 33));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E2, true, true, false>, true, false, false, 1, false, true>(FK_VARIANT_EO, 34));
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, true, true, false>, true, false, false, 1, true, true>(FK_VARIANT_EO, 35));
+  out.push_back(entry<FK_VARIANT_EO, 33, D, Q, NC, TunedEo<D, Q, NC, E2, false, true, false>, true, false, false, 1, true, true>());
+  out.push_back(entry<FK_VARIANT_EO, 34, D, Q, NC, TunedEo<D, Q, NC, E2, true, true, false>, true, false, false, 1, false, true>());
+  out.push_back(entry<FK_VARIANT_EO, 35, D, Q, NC, TunedEo<D, Q, NC, E1, true, true, false>, true, false, false, 1, true, true>());
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;
   using M1 = TunedEo<D, Q, NC, E1, false, true>;
@@ -169,21 +187,21 @@ void add_all(std::vector<KernelEntry>& out) {
   using M1s = TunedEo<D, Q, NC, E1, false, false>;
   using M2is = TunedEo<D, Q, NC, E2, true, false>;
   using M0is = TunedEo<D, Q, NC, E0, true, false>;
-  out.push_back(entry<D, Q, NC, M2, true, false, true>(FK_VARIANT_MF, 0));
-  out.push_back(entry<D, Q, NC, M1, true, false, true>(FK_VARIANT_MF, 1));
-  out.push_back(entry<D, Q, NC, M2i, true, false, true>(FK_VARIANT_MF, 2));
-  out.push_back(entry<D, Q, NC, M0i, true, false, true>(FK_VARIANT_MF, 3));
-  out.push_back(entry<D, Q, NC, M2s, true, false, true>(FK_VARIANT_MF, 4));
-  out.push_back(entry<D, Q, NC, M1s, true, false, true>(FK_VARIANT_MF, 5));
-  out.push_back(entry<D, Q, NC, M2is, true, false, true>(FK_VARIANT_MF, 6));
-  out.push_back(entry<D, Q, NC, M0is, true, false, true>(FK_VARIANT_MF, 7));
+  out.push_back(entry<FK_VARIANT_MF, 0, D, Q, NC, M2, true, false, true>());
+  out.push_back(entry<FK_VARIANT_MF, 1, D, Q, NC, M1, true, false, true>());
+  out.push_back(entry<FK_VARIANT_MF, 2, D, Q, NC, M2i, true, false, true>());
+  out.push_back(entry<FK_VARIANT_MF, 3, D, Q, NC, M0i, true, false, true>());
+  out.push_back(entry<FK_VARIANT_MF, 4, D, Q, NC, M2s, true, false, true>());
+  out.push_back(entry<FK_VARIANT_MF, 5, D, Q, NC, M1s, true, false, true>());
+  out.push_back(entry<FK_VARIANT_MF, 6, D, Q, NC, M2is, true, false, true>());
+  out.push_back(entry<FK_VARIANT_MF, 7, D, Q, NC, M0is, true, false, true>());
   // mf8-9: closed-form ids (GM 1) and precomputed gather slots (XP); with the
   // static-table three-component bodies XP costs registers, so BP1 only gains
   // (profiles/r01_sweep_v20_mf_xp.jsonl)
-  out.push_back(entry<D, Q, NC, M1s, true, false, true, 1, false, true>(FK_VARIANT_MF, 8));
-  out.push_back(entry<D, Q, NC, M0is, true, false, true, 1, false, true>(FK_VARIANT_MF, 9));
+  out.push_back(entry<FK_VARIANT_MF, 8, D, Q, NC, M1s, true, false, true, 1, false, true>());
+  out.push_back(entry<FK_VARIANT_MF, 9, D, Q, NC, M0is, true, false, true, 1, false, true>());
   // mf10: the BP3 p=4 PA default's body (cfg 35) without the PA stream
-  out.push_back(entry<D, Q, NC, TunedEo<D, Q, NC, E1, true, true, false>, true, false, true, 1, true, true>(FK_VARIANT_MF, 10));
+  out.push_back(entry<FK_VARIANT_MF, 10, D, Q, NC, TunedEo<D, Q, NC, E1, true, true, false>, true, false, true, 1, true, true>());
 }
 
 }  // namespace

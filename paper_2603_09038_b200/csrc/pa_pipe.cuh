@@ -72,7 +72,11 @@ struct HasQf {
 };
 template <class B>
 struct HasQf<B, decltype((void)B::QF_OK)> {
+#ifdef FK_NO_QF
+  static constexpr bool value = false;  // A/B builds without the quadratic form
+#else
   static constexpr bool value = B::QF_OK;
+#endif
 };
 
 __device__ __forceinline__ int fast_div(int n, unsigned m, int s) {
@@ -109,7 +113,7 @@ struct PipeSmem {
 // no id array traffic, one int per element per slot.  SX: a single X buffer;
 // the next batch's gather is issued after stage A has consumed the current one.
 template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false, bool MF = false, int GM = 0,
-          bool SX = false, bool XP = false>
+          bool SX = false, bool XP = false, bool QF = false>
 __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ typename Body::Tab tb,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
@@ -305,9 +309,11 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   wait_g(0);
   issue_x(blockIdx.x, 0, xb);
 
-  // element quadratic form (CG's p.Ap): per-thread partial in a register
+  // element quadratic form (QF instances only: CG's p.Ap), per-thread partial
+  // in a register; without QF the pointer is a compile-time null and stage C
+  // carries no trace of it
   double qacc = 0.0;
-  double* const qptr = sid.qf ? &qacc : nullptr;
+  double* const qptr = QF ? &qacc : nullptr;
   auto run_batch = [&](int b, int it) {
     const int gslot = it % NG;
     double* xcur = SX ? xb : xb + (it & 1) * E * XS;
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     }
     Body::stage_b(tb, it, s1, s0, ne, ex);
     __syncthreads();
-    if constexpr (HasQf<Body>::value) {
+    if constexpr (QF && HasQf<Body>::value) {
       if constexpr (MF) {
         Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex, qptr);
       } else if constexpr (DG) {
@@ -383,8 +389,8 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     // basis-table loads out of (co-resident CTAs overlap load and compute)
     run_batch(blockIdx.x, 0);
   }
-  if constexpr (HasQf<Body>::value) {
-    if (sid.qf) {  // CTA partial of the quadratic form, fixed reduction order
+  if constexpr (QF && HasQf<Body>::value) {
+    {  // CTA partial of the quadratic form, fixed reduction order
       __shared__ double qw[(T + 31) / 32];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) qacc += __shfl_down_sync(0xffffffffu, qacc, o);
