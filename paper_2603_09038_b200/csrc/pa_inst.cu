@@ -14,6 +14,7 @@
 #include "pa_dfma_eo.cuh"
 #include "pa_eo_layouts.cuh"
 #include "pa_dmma.cuh"
+#include "pa_dmma_map.cuh"
 #include "pa_pipe.cuh"
 
 #ifndef FK_P
@@ -145,6 +146,14 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<FK_VARIANT_DMMA, 0, D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true>());
   out.push_back(entry<FK_VARIANT_DMMA, 1, D, Q, NC, DmmaBody<D, Q, NC, E0, 256>, true>());
   out.push_back(entry<FK_VARIANT_DMMA, 2, D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true, true>());
+  // cfgs 3-5: the paper's per-element DMMA dataflow on the reference's shipped
+  // conflict-free tile maps (pa_dmma_map.cuh): p = 3, q = 5 only, 1 / 2 / 4
+  // elements (4 warps each) per CTA
+  if constexpr (D == 4 && Q == 5) {
+    out.push_back(entry<FK_VARIANT_DMMA, 3, D, Q, NC, DmmaMapBody<NC, 1>, true>());
+    out.push_back(entry<FK_VARIANT_DMMA, 4, D, Q, NC, DmmaMapBody<NC, 2>, true>());
+    out.push_back(entry<FK_VARIANT_DMMA, 5, D, Q, NC, DmmaMapBody<NC, 4>, true>());
+  }
   using F0 = DfmaBody<D, Q, NC, E0, round32(E0 * Q * Q), 1>;
   out.push_back(entry<FK_VARIANT_DFMA, 6, D, Q, NC, F0, true>());
   // even-odd bodies.  cfg 0: the line layout of the first EO kernels (reference
