@@ -358,6 +358,11 @@ def init_ranks(a):
         return world, rank, local, None, None
     import torch.distributed as dist
 
+    # NCCL's init log (ranks, devices, NVLink/NVLS topology) to stderr, so the
+    # rank count can be checked while stdout keeps its single JSON line
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if shared is not None:
         dist.init_process_group("gloo")
     else:
