@@ -146,6 +146,11 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<FK_VARIANT_DMMA, 0, D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true>());
   out.push_back(entry<FK_VARIANT_DMMA, 1, D, Q, NC, DmmaBody<D, Q, NC, E0, 256>, true>());
   out.push_back(entry<FK_VARIANT_DMMA, 2, D, Q, NC, DmmaBody<D, Q, NC, E1, 128>, true, true>());
+  // cfgs 6-8: smaller footprints for occupancy (D via L2): one element per CTA
+  // with 4 or 8 warps, two elements with 8 warps
+  out.push_back(entry<FK_VARIANT_DMMA, 6, D, Q, NC, DmmaBody<D, Q, NC, 1, 128>, true, true>());
+  out.push_back(entry<FK_VARIANT_DMMA, 7, D, Q, NC, DmmaBody<D, Q, NC, 1, 256>, true, true>());
+  out.push_back(entry<FK_VARIANT_DMMA, 8, D, Q, NC, DmmaBody<D, Q, NC, E1, 256>, true, true>());
   // cfgs 3-5: the paper's per-element DMMA dataflow on the reference's shipped
   // conflict-free tile maps (pa_dmma_map.cuh): p = 3, q = 5 only, 1 / 2 / 4
   // elements (4 warps each) per CTA
