@@ -392,6 +392,8 @@ def run_ours(a):
     mesh = build_mesh(n, n, n * world)
     op = PAOperator(mesh, p, q, kind=a.kind, variant=a.variant, comm=comm,
                     deterministic=a.deterministic)
+    if comm is not None:
+        print(f"[fk] rank {rank}: exchange transport in use: {comm.transport}", file=sys.stderr, flush=True)
     rng = np.random.default_rng(rank)
     x = torch.as_tensor(rng.standard_normal(op.num_dofs), device="cuda")
     y = torch.empty_like(x)
@@ -510,7 +512,7 @@ def run_ours(a):
         # kernels of ours per apply: the fused kernel (3 launches: two boundary
         # layers + interior, when a multi-rank slab has >= 3 layers) and the
         # four exchange kernels (credit wait, put, arrival wait, add)
-        per_apply = 1 if world == 1 else ((3 if n >= 3 else 1) + (4 if a.transport == "p2p" else 2))
+        per_apply = 1 if world == 1 else ((3 if n >= 3 else 1) + (4 if comm.transport == "p2p" else 2))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -519,7 +521,7 @@ def run_ours(a):
             "config": workload_config(a.kind, p, q, n, world),
             "impl_config": {
                 "variant": op.variant, "cfg": op.info.cfg, "dofs_per_gpu": op.num_dofs,
-                "transport": a.transport if world > 1 else None,
+                "transport": comm.transport if comm is not None else None,
                 "deterministic": a.deterministic,
                 "l2": ((f"inputs larger than L2 ({op.bytes_per_apply / 1e9:.2f} GB moved "
                         "per apply, no flush needed)") if op.bytes_per_apply > 126e6 else
@@ -669,7 +671,7 @@ def run_cg(a):
                        "mesh": list(dims), "p": p, "q": p + 2, "iterations": iters,
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
             "impl_config": {"variant": op.variant, "cfg": op.info.cfg, "dofs_per_gpu": op.num_dofs,
-                            "transport": a.transport if world > 1 else None,
+                            "transport": comm.transport if comm is not None else None,
                             "deterministic": a.deterministic},
             "cpu_baseline": cpu,
             "clocks": sampler.summary(),

@@ -447,6 +447,8 @@ class Comm:
     rank attaches collectively, as it constructs its operator).
     ``transport="nccl"``: grouped ncclSend/ncclRecv + ncclAllReduce; the
     128-byte ncclUniqueId is produced by rank 0 and broadcast over ``group``.
+    If the CUDA-IPC mapping fails on any rank (no peer access on some pair),
+    all ranks agree and fall back to NCCL (``fallback=False``: raise).
 
     ``Comm.loopback(n, plane_cap, devices)`` builds n ranks inside this
     process, one per GPU; drive each rank from its own thread and stream
@@ -458,7 +460,7 @@ class Comm:
     preemption and always progress (tests/_rankpool.py)."""
 
     def __init__(self, rank: int, world_size: int, device: int, group=None,
-                 transport: str = "p2p", plane_cap: int | None = None):
+                 transport: str = "p2p", plane_cap: int | None = None, fallback: bool = True):
         if transport not in _lib.TRANSPORTS:
             raise ValueError(f"transport must be one of {tuple(_lib.TRANSPORTS)}, got {transport!r}")
         if not 0 <= rank < world_size:
@@ -467,21 +469,11 @@ class Comm:
         self.rank, self.world_size, self.device = rank, world_size, device
         self.transport = transport
         self.group = group
+        self.fallback = bool(fallback)
         self.handle = None
         self.plane_cap = None
         if transport == "nccl":
-            import torch.distributed as dist
-
-            uid = (ctypes.c_char * 128)()
-            if rank == 0:
-                _lib.check(self._lib.fk_comm_unique_id(uid))
-            payload = [bytes(uid)]
-            if world_size > 1:
-                dist.broadcast_object_list(payload, src=0, group=group)
-            uid = (ctypes.c_char * 128).from_buffer_copy(payload[0])
-            h = ctypes.c_void_p()
-            _lib.check(self._lib.fk_comm_create(ctypes.byref(h), uid, rank, world_size, device))
-            self.handle = h
+            self._create_nccl()
         elif plane_cap is not None:
             self._create_p2p(int(plane_cap))
 
@@ -498,9 +490,41 @@ class Comm:
             dist.all_gather_object(handles, bytes(mine), group=self.group)
             blob = (ctypes.c_char * (_lib.FK_IPC_HANDLE_BYTES * self.world_size)).from_buffer_copy(
                 b"".join(handles))
-            _lib.check(self._lib.fk_comm_connect_p2p(self.handle, blob))
+            rc = self._lib.fk_comm_connect_p2p(self.handle, blob)
+            err = self._lib.fk_last_error().decode(errors="replace") if rc else ""
+            # agree on the outcome: a node without peer access on some pair
+            # falls back to NCCL on every rank together
+            oks = [None] * self.world_size
+            dist.all_gather_object(oks, rc == _lib.FK_OK, group=self.group)
+            if not all(oks):
+                self._lib.fk_comm_destroy(self.handle)
+                self.handle = None
+                if not self.fallback:
+                    raise _lib.FkError(_lib.FK_ECUDA, f"P2P mailboxes could not be mapped: {err}")
+                import warnings
+
+                warnings.warn(f"rank {self.rank}: CUDA-IPC peer mapping failed ({err or 'on a peer'}); "
+                              "falling back to the NCCL transport")
+                self.transport = "nccl"
+                self._create_nccl()
+                return
             # every rank's mappings exist before any rank stores into a peer
             dist.barrier(group=self.group)
+
+    def _create_nccl(self) -> None:
+        import torch.distributed as dist
+
+        uid = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            _lib.check(self._lib.fk_comm_unique_id(uid))
+        payload = [bytes(uid)]
+        if self.world_size > 1:
+            dist.broadcast_object_list(payload, src=0, group=self.group)
+        uid = (ctypes.c_char * 128).from_buffer_copy(payload[0])
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.fk_comm_create(ctypes.byref(h), uid, self.rank, self.world_size,
+                                            self.device))
+        self.handle = h
 
     @classmethod
     def loopback(cls, nranks: int, plane_cap: int, devices=None) -> list["Comm"]:
