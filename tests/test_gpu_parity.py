@@ -422,3 +422,23 @@ def test_reference_objects_drop_in(golden):
     op = PAOperator(RefLikeMesh(), 4, basis=b)
     y = op.apply(dev(golden["bp3_3x3x3_p4_x"])).cpu().numpy()
     assert normwise(y, golden["bp3_3x3x3_p4_y"]) <= PARITY_TOL
+
+
+@pytest.mark.parametrize("p,n,variant,iters", [
+    (6, (3, 3, 3), "auto", 60),   # BASELINE configs[4] order
+    (6, (2, 3, 4), "mf", 60),     # matrix-free operator, as bench.py --cg ... --variant mf
+    (4, (3, 3, 3), "mf", 80),
+    (8, (2, 2, 2), "auto", 40),
+    (5, (3, 2, 3), "dmma", 40),   # a non-QF kernel: p.Ap by the dot pass
+])
+def test_cg_more_orders_and_variants(p, n, variant, iters):
+    """CG on the fused iteration (p.Ap as the kernel's element quadratic form
+    for EO / MF geometries, the dot pass otherwise) against the oracle PCG."""
+    P = bp.Problem("diffusion", *n, p)
+    op = make("diffusion", n, p, dirichlet=True, variant=variant)
+    b = np.random.default_rng(p).standard_normal(P.ndof)
+    b[P.boundary()] = 0.0
+    x, h = cg_solve(op, b, iters=iters)
+    xr, hr = P.pcg(b, iters=iters)
+    assert len(h) == len(hr) and np.max(np.abs(h - hr)) <= 1e-8 * hr[0]
+    assert normwise(x, xr) <= 1e-8
