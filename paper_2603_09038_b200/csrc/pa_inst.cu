@@ -15,6 +15,7 @@
 #include "pa_eo_layouts.cuh"
 #include "pa_dmma.cuh"
 #include "pa_dmma_map.cuh"
+#include "pa_dmma_warp.cuh"
 #include "pa_pipe.cuh"
 
 #ifndef FK_P
@@ -64,6 +65,38 @@ void launch_diag(const OpView& v, double* diag, int64_t nel, int blocks, cudaStr
   std::memcpy(tb.G, v.G, sizeof(tb.G));
   diagonal_kernel<D, Q, NC><<<blocks, 128, 0, s>>>(tb, diag, v.gids, v.pa, nel);
 }
+
+template <int D, int Q, int NC, int W>
+void launch_warp_dmma(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
+  Tables<D, Q> tb;
+  std::memcpy(tb.B, v.B, sizeof(tb.B));
+  std::memcpy(tb.G, v.G, sizeof(tb.G));
+  const StructIds sid = struct_ids(v);
+  dmma_warp_kernel<D, Q, NC, W><<<blocks, 32 * W, WarpDmmaKernel<D, Q, NC, W>::SMEM, s>>>(
+      tb, x, y, v.pa, v.ebits, v.nel, sid);
+}
+
+// warp-per-element DMMA (pa_dmma_warp.cuh): closed-form ids, D through L2
+template <int D, int Q, int NC, int W>
+KernelEntry warp_dmma_entry(int cfg) {
+  KernelEntry k;
+  k.nc = NC;
+  k.d = D;
+  k.q = Q;
+  k.variant = FK_VARIANT_DMMA;
+  k.cfg = cfg;
+  k.E = W;
+  k.T = 32 * W;
+  k.persist = true;
+  k.structured = true;
+  k.smem = WarpDmmaKernel<D, Q, NC, W>::SMEM;
+  k.func = reinterpret_cast<const void*>(&dmma_warp_kernel<D, Q, NC, W>);
+  k.launch = &launch_warp_dmma<D, Q, NC, W>;
+  k.diag = &launch_diag<D, Q, NC>;
+  k.diag_func = reinterpret_cast<const void*>(&diagonal_kernel<D, Q, NC>);
+  return k;
+}
+
 
 // Geometries that CG may select (fk_api.cu: kAutoCfg3 / kAutoCfgMF3 for q = p+2
 // and the array-map tables of the deterministic mode) get a twin instance with
@@ -151,6 +184,12 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<FK_VARIANT_DMMA, 6, D, Q, NC, DmmaBody<D, Q, NC, 1, 128>, true, true>());
   out.push_back(entry<FK_VARIANT_DMMA, 7, D, Q, NC, DmmaBody<D, Q, NC, 1, 256>, true, true>());
   out.push_back(entry<FK_VARIANT_DMMA, 8, D, Q, NC, DmmaBody<D, Q, NC, E1, 256>, true, true>());
+  // cfgs 9-11: one warp per element, stages chained in registers (d, q <= 8)
+  if constexpr (D <= 8 && Q <= 8) {
+    out.push_back(warp_dmma_entry<D, Q, NC, 4>(9));
+    out.push_back(warp_dmma_entry<D, Q, NC, 8>(10));
+    out.push_back(warp_dmma_entry<D, Q, NC, 2>(11));
+  }
   // cfgs 3-5: the paper's per-element DMMA dataflow on the reference's shipped
   // conflict-free tile maps (pa_dmma_map.cuh): p = 3, q = 5 only, 1 / 2 / 4
   // elements (4 warps each) per CTA
