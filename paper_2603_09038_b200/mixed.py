@@ -192,17 +192,33 @@ class MixedOperator:
     def apply(self, state, out: State | None = None) -> State:
         """Residual of the coupling operator acting on [u, p] (operator.py:331-362)."""
         self._check(state)
+        torch = _torch()
+        host_out = out is not None and isinstance(out.u, np.ndarray)
+        if out is not None:
+            self._check(out)
+            for name, a in (("out.u", out.u), ("out.p", out.p)):
+                if isinstance(a, np.ndarray):
+                    if a.dtype != np.float64 or not a.flags.c_contiguous or not a.flags.writeable:
+                        raise ValueError(f"{name} must be a writeable C-contiguous float64 array")
+                elif a.dtype != torch.float64 or a.device != self.device or not a.is_contiguous():
+                    raise ValueError(f"{name} must be a contiguous float64 tensor on {self.device}")
         self._count(1)
         host = isinstance(state.u, np.ndarray)
         u, p = self._dev(state.u), self._dev(state.p)
-        torch = _torch()
-        ou = torch.empty_like(u) if out is None else self._dev(out.u)
-        op = torch.empty_like(p) if out is None else self._dev(out.p)
+        dev_out = out is not None and not host_out
+        ou = self._dev(out.u) if dev_out else torch.empty_like(u)
+        op = self._dev(out.p) if dev_out else torch.empty_like(p)
         _lib.check(self._lib.fk_mix_apply(self._h, u.data_ptr(), p.data_ptr(), ou.data_ptr(),
                                           op.data_ptr()))
+        if host_out:  # NumPy out buffers are filled in place
+            out.u[...] = ou.cpu().numpy()
+            out.p[...] = op.cpu().numpy()
+            return out
+        if dev_out:
+            return out
         if host:
             return State(ou.cpu().numpy(), op.cpu().numpy())
-        return State(ou, op) if out is None else out
+        return State(ou, op)
 
     __call__ = apply
 

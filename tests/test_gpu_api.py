@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 from oracle import bp
-from paper_2603_09038_b200 import Counters, MixedOperator, PAOperator, cg_solve, fem
+from paper_2603_09038_b200 import Counters, MixedOperator, MixedState, PAOperator, cg_solve, fem
 
 pytestmark = pytest.mark.gpu
 
@@ -103,3 +103,21 @@ def test_diagonal_closed_form_and_general_kernel_agree(kind, p):
     scale = np.abs(ref).max()
     assert np.abs(box - ref).max() <= 1e-13 * scale
     assert np.abs(gen - ref).max() <= 1e-13 * scale
+
+
+def test_mixed_apply_fills_host_out_in_place():
+    op = MixedOperator(fem.build_mesh(2, 2, 2))
+    rng = np.random.default_rng(0)
+    s = MixedState(rng.standard_normal(op.u_shape), rng.standard_normal(op.num_p))
+    ref = op.apply(s)
+    out = MixedState(np.empty(op.u_shape), np.empty(op.num_p))
+    assert op.apply(s, out=out) is out
+    assert np.array_equal(out.u, ref.u) and np.array_equal(out.p, ref.p)
+    with pytest.raises(ValueError):
+        op.apply(s, out=MixedState(np.empty(op.u_shape, np.float32), np.empty(op.num_p)))
+    with pytest.raises(ValueError, match="do not match"):
+        op.apply(s, out=MixedState(np.empty((3, 1, 1)), np.empty(op.num_p)))
+    dev = MixedState(torch.empty(op.u_shape, dtype=torch.float64, device="cuda"),
+                     torch.empty(op.num_p, dtype=torch.float64, device="cuda"))
+    assert op.apply(s, out=dev) is dev
+    assert np.array_equal(dev.u.cpu().numpy(), ref.u)
