@@ -720,6 +720,18 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
     const double t = (double)c / K, f = ramp ? t * t * (3.0 - 2.0 * t) : t;
     return std::min(nzl, std::max(1, (int)std::lround(f * nzl)));
   };
+  // FK_HOST_TRACE=1: timing events per chunk and stream, printed to stderr
+  // (tools/pcie_probe.py; diagnosis only)
+  const bool trace = std::getenv("FK_HOST_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t s) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    tev.push_back(e);
+  };
+  tmark(op->stream);
   for (int c = 0; c < K; ++c) {
     const int z0 = zb(c), z1 = zb(c + 1);
     if (z1 <= z0) continue;
@@ -727,18 +739,36 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
     FK_CUDA(cudaMemcpyAsync(op->stage_x + x_done * P, xh + x_done * P,
                             sizeof(double) * (x_hi - x_done) * P, cudaMemcpyHostToDevice, op->h2d));
     x_done = x_hi;
+    tmark(op->h2d);
     FK_CUDA(cudaEventRecord(op->chunk_ev[2 * c], op->h2d));
     FK_CUDA(cudaStreamWaitEvent(op->stream, op->chunk_ev[2 * c], 0));
+    tmark(op->stream);
     FK_TRY(launch_range(op, op->stage_x, op->stage_y, (int64_t)z0 * nxy, (int64_t)(z1 - z0) * nxy,
                         op->stream));
+    tmark(op->stream);
     FK_CUDA(cudaEventRecord(op->chunk_ev[2 * c + 1], op->stream));
     FK_CUDA(cudaStreamWaitEvent(op->d2h, op->chunk_ev[2 * c + 1], 0));
     const int64_t y_hi = (z1 == nzl) ? op->npz_local : (int64_t)z1 * p;
     FK_CUDA(cudaMemcpyAsync(yh + y_done * P, op->stage_y + y_done * P,
                             sizeof(double) * (y_hi - y_done) * P, cudaMemcpyDeviceToHost, op->d2h));
     y_done = y_hi;
+    tmark(op->d2h);
   }
   FK_CUDA(cudaStreamSynchronize(op->d2h));
+  if (trace) {
+    cudaDeviceSynchronize();
+    std::string line = "[fk host trace ms] ";
+    for (size_t i = 1; i < tev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      const char* kind = (i - 1) % 4 == 0 ? "h2d" : (i - 1) % 4 == 1 ? "cs" : (i - 1) % 4 == 2 ? "ce" : "d2h";
+      char b[48];
+      snprintf(b, sizeof(b), "%s%zu=%.3f ", kind, (i - 1) / 4, ms);
+      line += b;
+    }
+    fprintf(stderr, "%s\n", line.c_str());
+    for (auto e : tev) cudaEventDestroy(e);
+  }
   return FK_OK;
 }
 
