@@ -320,7 +320,7 @@ static int preload_kernels(const fk_op* op) {
                       reinterpret_cast<const void*>(&fk::cg_step_kernel),
                       reinterpret_cast<const void*>(&fk::qf_sum_kernel),
                       reinterpret_cast<const void*>(&fk::recip_kernel),
-                      reinterpret_cast<const void*>(&fk::diag_box_kernel)};
+                      reinterpret_cast<const void*>(&fk::diag_box_rn_kernel)};
   cudaFuncAttributes a;
   for (const void* k : ks) FK_CUDA(cudaFuncGetAttributes(&a, k));
   for (const auto& k : registry()) {
@@ -772,60 +772,86 @@ int fk_op_apply_host(fk_op* op, const double* xh, double* yh) {
   return FK_OK;
 }
 
+// 1D factor tables of the closed-form box diagonal (fk_cg.cuh BoxDiag):
+// f(i) = sum_a w_a T[a][i]^2 (T = B, G), assembled over the elements holding
+// a node: x and y over the box, z over the GLOBAL element layers at this
+// rank's planes (a shared plane gets both layers' contributions on both ranks)
+static int ensure_box_tab(fk_op* op) {
+  if (op->diag_tab != nullptr) return FK_OK;
+  const int d = op->d, q = op->q, p = op->p;
+  double fb[9] = {}, fg[9] = {};
+  for (int i = 0; i < d; ++i)
+    for (int a = 0; a < q; ++a) {
+      fb[i] += op->w[a] * (op->B[a * d + i] * op->B[a * d + i]);
+      fg[i] += op->w[a] * (op->G[a * d + i] * op->G[a * d + i]);
+    }
+  const int64_t z0p = (int64_t)op->desc.z0_layer * p;
+  std::vector<double> h(2 * (op->npx + op->npy + op->npz_local), 0.0);
+  auto assemble = [&](double* out, int64_t n, int64_t g0, int64_t nglob, const double* f) {
+    for (int64_t l = 0; l < n; ++l) {
+      const int64_t g = g0 + l;
+      double v = 0.0;
+      if (g % p != 0) v = f[g % p];
+      else {
+        if (g > 0) v += f[p];
+        if (g < nglob - 1) v += f[0];
+      }
+      out[l] = v;
+    }
+  };
+  double* t = h.data();
+  assemble(t, op->npx, 0, op->npx, fb);
+  assemble(t + op->npx, op->npx, 0, op->npx, fg);
+  t += 2 * op->npx;
+  assemble(t, op->npy, 0, op->npy, fb);
+  assemble(t + op->npy, op->npy, 0, op->npy, fg);
+  t += 2 * op->npy;
+  assemble(t, op->npz_local, z0p, op->npz_global, fb);
+  assemble(t + op->npz_local, op->npz_local, z0p, op->npz_global, fg);
+  FK_CUDA(cudaMalloc(&op->diag_tab, sizeof(double) * h.size()));
+  FK_CUDA(cudaMemcpyAsync(op->diag_tab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
+                          op->stream));
+  FK_CUDA(cudaStreamSynchronize(op->stream));
+  return FK_OK;
+}
+
+static void div_magic32(int d, unsigned& m, int& s) {
+  s = 0;
+  while ((1ll << s) < d) ++s;
+  m = (unsigned)((((1ull << 32) * ((1ull << s) - (unsigned long long)d)) / (unsigned long long)d) + 1);
+}
+
+static fk::BoxDiag box_diag(const fk_op* op) {
+  fk::BoxDiag b;
+  b.tab = op->diag_tab;
+  b.npx = (int)op->npx;
+  b.npy = (int)op->npy;
+  b.npz = (int)op->npz_local;
+  b.nc = op->nc;
+  const double dj = op->desc.jac_det;
+  b.c0 = dj * (op->jinv[0] * op->jinv[0]);
+  b.c1 = dj * (op->jinv[1] * op->jinv[1]);
+  b.c2 = dj * (op->jinv[2] * op->jinv[2]);
+  b.cm = dj;
+  b.dirichlet = op->desc.dirichlet ? 1 : 0;
+  b.z0p = op->desc.z0_layer * op->p;
+  b.npzg = (int)op->npz_global;
+  div_magic32(b.npx, b.mx, b.sx);
+  div_magic32(b.npy, b.my, b.sy);
+  return b;
+}
+
 int fk_op_diagonal(fk_op* op, double* diag) {
   if (op == nullptr || diag == nullptr) return fail(FK_EINVAL, "null argument");
   if (!op->is_setup) return fail(FK_EINVAL, "fk_op_setup has not been called");
   DeviceGuard g(op->device);
   if (op->host_gids.empty()) {
-    // structured box: separable closed form, one pass (fk_setup.cuh diag_box_kernel)
-    if (op->diag_tab == nullptr) {
-      const int64_t np3 = op->npx + op->npy + op->npz_local;
-      std::vector<double> h(2 * np3, 0.0);
-      const int d = op->d, q = op->q, p = op->p;
-      double fb[9] = {}, fg[9] = {};
-      for (int i = 0; i < d; ++i)
-        for (int a = 0; a < q; ++a) {
-          fb[i] += op->w[a] * (op->B[a * d + i] * op->B[a * d + i]);
-          fg[i] += op->w[a] * (op->G[a * d + i] * op->G[a * d + i]);
-        }
-      // assembled 1D factor over n elements: node g takes f(g % p) from the
-      // element on its left (local index p when g % p == 0) and on its right
-      auto assemble = [&](double* out, int64_t npn, const double* f) {
-        for (int64_t g = 0; g < npn; ++g) {
-          double v = 0.0;
-          if (g % p != 0) v = f[g % p];
-          else {
-            if (g > 0) v += f[p];
-            if (g < npn - 1) v += f[0];
-          }
-          out[g] = v;
-        }
-      };
-      double* t = h.data();
-      assemble(t, op->npx, fb);
-      assemble(t + op->npx, op->npx, fg);
-      t += 2 * op->npx;
-      assemble(t, op->npy, fb);
-      assemble(t + op->npy, op->npy, fg);
-      t += 2 * op->npy;
-      assemble(t, op->npz_local, fb);
-      assemble(t + op->npz_local, op->npz_local, fg);
-      FK_CUDA(cudaMalloc(&op->diag_tab, sizeof(double) * h.size()));
-      FK_CUDA(cudaMemcpyAsync(op->diag_tab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
-                              op->stream));
-      FK_CUDA(cudaStreamSynchronize(op->stream));
-    }
-    const double dj = op->desc.jac_det;
-    fk::diag_box_kernel<<<grid_for(op->ndof, 256, op->num_sms), 256, 0, op->stream>>>(
-        diag, op->diag_tab, op->npx, op->npy, op->npz_local, op->nc, dj * (op->jinv[0] * op->jinv[0]),
-        dj * (op->jinv[1] * op->jinv[1]), dj * (op->jinv[2] * op->jinv[2]), dj);
+    // structured box: separable closed form, one pass, no atomics and no
+    // exchange (the z factor is assembled over the global layers)
+    FK_TRY(ensure_box_tab(op));
+    fk::diag_box_rn_kernel<<<grid_for(op->ndof, 256, op->num_sms), 256, 0, op->stream>>>(
+        diag, box_diag(op), op->ndof);
     FK_CUDA(cudaGetLastError());
-    if (op->comm) FK_TRY(fk::exchange_interface(op, diag, op->stream));
-    if (op->desc.dirichlet && op->n_ess > 0) {
-      fk::ess_set_kernel<<<grid_for(op->n_ess, 256, op->num_sms), 256, 0, op->stream>>>(
-          diag, op->ess, op->n_ess, 1.0);
-      FK_CUDA(cudaGetLastError());
-    }
     return FK_OK;
   }
   FK_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * op->ndof, op->stream));

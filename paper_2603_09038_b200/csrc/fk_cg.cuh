@@ -172,6 +172,60 @@ __global__ void cg_step_kernel(double* __restrict__ x, double* __restrict__ p,
   }
 }
 
+// ---- closed-form Jacobi on the box (fk_op_diagonal's box path, fk_setup.cuh) ----
+// diag(gi, gj, gk) = sum_s c_s F^x_s(gi) F^y_s(gj) F^z_s(gk) from host-built
+// 1D factor tables (the z table assembled over the GLOBAL element layers, so
+// shared planes need no exchange and every rank holds the same bits), with
+// every product and sum rounded separately (no FMA contraction: the result
+// does not depend on the compiler's choices); 1 on the essential (box-face)
+// dofs.  (Computing dinv inside the CG passes from these tables instead of
+// reading a dinv vector was measured slower: the FP64 division and the index
+// decomposition cost more than the 16 B/dof they save.)
+struct BoxDiag {
+  const double* tab;  // [FBx FGx | FBy FGy | FBz FGz], z over the rank's planes
+  int npx, npy, npz;  // local planes
+  int nc;
+  double c0, c1, c2, cm;
+  int dirichlet;
+  int z0p, npzg;      // first global plane of the rank, global planes
+  unsigned mx, my;    // fast division by npx, npy (pa_pipe.cuh fast_div)
+  int sx, sy;
+};
+
+__device__ __forceinline__ double box_diag_at(const BoxDiag& b, int i, int j, int k) {
+  const double* bx = b.tab;
+  const double* gx = bx + b.npx;
+  const double* by = gx + b.npx;
+  const double* gy = by + b.npy;
+  const double* bz = gy + b.npy;
+  const double* gz = bz + b.npz;
+  if (b.nc == 3) {
+    const double t0 = __dmul_rn(b.c0, __dmul_rn(__dmul_rn(gx[i], by[j]), bz[k]));
+    const double t1 = __dmul_rn(b.c1, __dmul_rn(__dmul_rn(bx[i], gy[j]), bz[k]));
+    const double t2 = __dmul_rn(b.c2, __dmul_rn(__dmul_rn(bx[i], by[j]), gz[k]));
+    return __dadd_rn(__dadd_rn(t0, t1), t2);
+  }
+  return __dmul_rn(b.cm, __dmul_rn(__dmul_rn(bx[i], by[j]), bz[k]));
+}
+
+__device__ __forceinline__ bool box_ess(const BoxDiag& b, int i, int j, int k) {
+  if (!b.dirichlet) return false;
+  const int kg = b.z0p + k;
+  return i == 0 || i == b.npx - 1 || j == 0 || j == b.npy - 1 || kg == 0 || kg == b.npzg - 1;
+}
+
+__global__ void diag_box_rn_kernel(double* __restrict__ diag, const BoxDiag b, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int tt = (int)t;
+    const int row = (int)((__umulhi((unsigned)tt, b.mx) + (unsigned)tt) >> b.sx);
+    const int i = tt - row * b.npx;
+    const int k = (int)((__umulhi((unsigned)row, b.my) + (unsigned)row) >> b.sy);
+    const int j = row - k * b.npy;
+    diag[t] = box_ess(b, i, j, k) ? 1.0 : box_diag_at(b, i, j, k);
+  }
+}
+
 __global__ void recip_kernel(double* __restrict__ out, const double* __restrict__ in, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)

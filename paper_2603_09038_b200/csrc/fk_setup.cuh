@@ -121,32 +121,4 @@ __global__ void ess_set_kernel(double* __restrict__ y, const int* __restrict__ e
     y[ess[t]] = v;
 }
 
-// Closed form on the structured box (the only mesh the reference builds,
-// mesh.py:78-120): D_ss(abc) = w_a w_b w_c |J| jinv_s^2 is separable and the
-// elements tile the box, so the ASSEMBLED diagonal factorises per direction:
-//   diag(gi, gj, gk) = sum_s c_s Fx_s(gi) Fy_s(gj) Fz_s(gk)      (BP3, c_s = |J| jinv_s^2)
-//   diag(gi, gj, gk) = |J| FxB(gi) FyB(gj) FzB(gk)               (BP1)
-// with F?_s = the assembled 1D factor sum over the elements holding the node
-// of f(i) = sum_a w_a T[a][i]^2 (T = G along direction s, B otherwise).  The
-// host builds the six 1D tables (fk_api.cu), this kernel is one write pass:
-// 8 B/dof, no atomics, deterministic.  tab = [FBx FGx | FBy FGy | FBz FGz].
-__global__ void diag_box_kernel(double* __restrict__ diag, const double* __restrict__ tab,
-                                int64_t npx, int64_t npy, int64_t npz, int nc, double c0, double c1,
-                                double c2, double cm) {
-  const double* bx = tab;
-  const double* gx = bx + npx;
-  const double* by = gx + npx;
-  const double* gy = by + npy;
-  const double* bz = gy + npy;
-  const double* gz = bz + npz;
-  const int64_t n = npx * npy * npz;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t % npx, jk = t / npx, j = jk % npy, k = jk / npy;
-    diag[t] = nc == 3 ? c0 * (gx[i] * by[j] * bz[k]) + c1 * (bx[i] * gy[j] * bz[k]) +
-                            c2 * (bx[i] * by[j] * gz[k])
-                      : cm * (bx[i] * by[j] * bz[k]);
-  }
-}
-
 }  // namespace fk

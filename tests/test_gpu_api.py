@@ -112,7 +112,9 @@ def test_mixed_apply_fills_host_out_in_place():
     ref = op.apply(s)
     out = MixedState(np.empty(op.u_shape), np.empty(op.num_p))
     assert op.apply(s, out=out) is out
-    assert np.array_equal(out.u, ref.u) and np.array_equal(out.p, ref.p)
+    # u is stored directly (bitwise); p is scattered with atomics (order varies)
+    assert np.array_equal(out.u, ref.u)
+    assert np.max(np.abs(out.p - ref.p)) <= 1e-14 * np.max(np.abs(ref.p))
     with pytest.raises(ValueError):
         op.apply(s, out=MixedState(np.empty(op.u_shape, np.float32), np.empty(op.num_p)))
     with pytest.raises(ValueError, match="do not match"):
@@ -121,3 +123,4 @@ def test_mixed_apply_fills_host_out_in_place():
                      torch.empty(op.num_p, dtype=torch.float64, device="cuda"))
     assert op.apply(s, out=dev) is dev
     assert np.array_equal(dev.u.cpu().numpy(), ref.u)
+    assert np.max(np.abs(dev.p.cpu().numpy() - ref.p)) <= 1e-14 * np.max(np.abs(ref.p))
