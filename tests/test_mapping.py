@@ -107,3 +107,34 @@ def test_shape_and_mapping_validation():
         mm.IndexMapping(mm.GemmShape(8, 8, 4), np.zeros((1, 7)), np.arange(8), np.arange(4))
     with pytest.raises(ValueError):
         mm.column_permuted_mapping(mm.GemmShape(8, 8, 4), [0, 1, 2, 3, 4, 5, 6, 6])
+
+
+def test_dmma_map_header_is_generated_from_the_shipped_maps(tmp_path, monkeypatch):
+    """csrc/pa_dmma_maps.cuh (consumed by the paper-style DMMA kernel,
+    pa_dmma_map.cuh) is exactly what tools/gen_dmma_maps.py produces from the
+    reference's shipped maps through this module, and each packed slot table
+    decodes back to the map."""
+    import importlib.util
+    import os
+    import re
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("gen_dmma_maps", os.path.join(root, "tools", "gen_dmma_maps.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    committed = open(gen.OUT).read()
+    out = tmp_path / "maps.cuh"
+    monkeypatch.setattr(gen, "OUT", str(out))
+    monkeypatch.setattr("sys.argv", ["gen_dmma_maps.py"])
+    gen.main()
+    assert out.read_text() == committed
+    for s in SHAPES:
+        mp = _shipped(s)
+        m = re.search(rf"struct Map<{mp.shape.m}, {mp.shape.n}, {mp.shape.k}> \{{.*?FN = 0x([0-9a-f]+)u, FK = 0x([0-9a-f]+)u;"
+                      r".*?return (.*?); \}", committed, re.S)
+        fn, fk = int(m.group(1), 16), int(m.group(2), 16)
+        assert [((fn >> (4 * i)) & 15) - 1 for i in range(mp.f_n.size)] == mp.f_n.tolist()
+        assert [((fk >> (4 * i)) & 15) - 1 for i in range(mp.f_k.size)] == mp.f_k.tolist()
+        words = [int(w, 16) for w in re.findall(r"0x([0-9a-f]+)ull", m.group(3))]
+        for w, row in enumerate(mp.f_m):
+            assert [((words[w] >> (5 * i)) & 31) - 1 for i in range(8)] == row.tolist()

@@ -98,3 +98,27 @@ def test_slab_exchange_matches_single_process(kind, n, p, world):
         assert err <= 1e-14  # normwise vs single process (summation order differs)
         assert dot_err <= 1e-13
         assert gerr <= 1e-13
+
+
+def test_bench_spawn_translates_n_for_torchrun(monkeypatch):
+    """bench.py --gpus N without torchrun re-launches itself under
+    torch.distributed.run; torchrun's parser would take '--n' as an
+    abbreviation of its own options, so it is passed as '--elems'."""
+    import importlib.util
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    seen = {}
+    monkeypatch.setattr(subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr("sys.argv", ["bench.py", "--gpus", "4", "--n", "24", "--steps", "3"])
+    a = bench.parse()
+    assert a.n == 24 and a.gpus == 4
+    bench.spawn_ranks(a)
+    cmd = seen["cmd"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    tail = cmd[cmd.index(os.path.abspath(os.path.join(root, "bench.py"))) + 1:]
+    assert tail == ["--gpus", "4", "--elems", "24", "--steps", "3"]
