@@ -164,7 +164,12 @@ int fk_dot(fk_op* op, const double* a_dev, const double* b_dev, double* host_out
  *                     ranks).  Kernel-only, so it is captured in the CG graph.
  *  FK_TRANSPORT_NCCL  grouped ncclSend/ncclRecv + ncclAllReduce.
  * nccl_unique_id points to the 128-byte ncclUniqueId produced by
- * fk_comm_unique_id on rank 0 and broadcast by the caller. */
+ * fk_comm_unique_id on rank 0 and broadcast by the caller.
+ * Ordering contract: every rank issues the same sequence of exchanges and
+ * reductions on a communicator (each operator call is collective), and one
+ * communicator's exchanges are issued in ONE stream order per rank (the P2P
+ * mailbox counters are per communicator); operators that share a
+ * communicator must not run exchanges concurrently on different streams. */
 #define FK_TRANSPORT_NCCL 1
 #define FK_TRANSPORT_P2P 2
 #define FK_MAX_RANKS 16
