@@ -21,10 +21,11 @@ def _ndof(n, p):
 
 
 class _Slab:
-    def __init__(self, rank, world, kind, n, p, transport="p2p", **kw):
+    def __init__(self, rank, world, kind, n, p, transport="p2p", extents=(1.0, 1.0, 1.0), q=None, **kw):
         self.comm = Comm(rank, world, 0, transport=transport)
         self.stream = torch.cuda.Stream()
-        self.op = PAOperator(fem.build_mesh(*n), p, kind=kind, comm=self.comm, stream=self.stream, **kw)
+        self.op = PAOperator(fem.build_mesh(*n, extents=extents), p, q, kind=kind, comm=self.comm,
+                             stream=self.stream, **kw)
         z0, z1 = self.comm.slab(n[2])
         self.lo, self.hi = parallel.local_dof_range(n[0], n[1], p, z0, z1)
 
@@ -42,9 +43,9 @@ class _Slab:
 
 
 def task_apply(rank, world, kind, n, p, dirichlet=False, seed=7, reps=3, variant="auto",
-               deterministic=False):
+               deterministic=False, extents=(1.0, 1.0, 1.0), q=None):
     s = _Slab(rank, world, kind, n, p, dirichlet=dirichlet, variant=variant,
-              deterministic=deterministic)
+              deterministic=deterministic, extents=extents, q=q)
     x = np.random.default_rng(seed).standard_normal(_ndof(n, p))
     xl = s.local(x)
     ys = []

@@ -196,3 +196,19 @@ def test_multirank_long_cg_protocol_stress(pools):
         assert np.array_equal(r["h"], res[0]["h"]) and len(r["h"]) == len(hr)
     # relative to the initial residual; late iterations sit at rounding level
     assert np.max(np.abs(res[0]["h"] - hr)) <= 1e-8 * hr[0]
+
+
+@pytest.mark.parametrize("kind,n,p,q,ext,world,variant", [
+    ("diffusion", (3, 2, 6), 3, 4, (2.0, 1.0, 0.5), 3, "auto"),   # q = p+1, anisotropic box
+    ("diffusion", (2, 3, 6), 4, 6, (1.0, 3.0, 2.0), 2, "mf"),     # matrix-free, anisotropic
+    ("mass", (3, 3, 6), 2, 3, (0.5, 1.0, 1.5), 3, "auto"),
+    ("diffusion", (2, 2, 8), 5, 7, (1.0, 1.0, 4.0), 4, "dmma"),   # batched DMMA kernel across ranks
+])
+def test_multirank_apply_anisotropic_and_q(pools, kind, n, p, q, ext, world, variant):
+    res = pools(world).run("apply", kind=kind, n=n, p=p, q=q, extents=ext, variant=variant,
+                           dirichlet=True)
+    P = bp.Problem(kind, *n, p, q, extents=ext)
+    x = np.random.default_rng(7).standard_normal(P.ndof)
+    ref = P.constrained_apply(x, P.boundary())
+    y = assemble(res, P.ndof, parallel.plane_size(n[0], n[1], p), "y")
+    assert normwise(y, ref) <= PARITY_TOL
