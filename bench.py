@@ -760,7 +760,7 @@ def run_sweep(a, peak):
     from paper_2603_09038_b200 import PAOperator, build_mesh
 
     out = []
-    cfgs = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(12)]
+    cfgs = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(15)]
             + [("eo", c) for c in range(36)] + [("mf", c) for c in range(11)])
     if a.sweep_cfgs:
         want = set(a.sweep_cfgs.split(","))

@@ -16,6 +16,7 @@
 #include "pa_dmma.cuh"
 #include "pa_dmma_map.cuh"
 #include "pa_dmma_warp.cuh"
+#include "pa_eo_dmmac.cuh"
 #include "pa_pipe.cuh"
 
 #ifndef FK_P
@@ -184,6 +185,23 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<FK_VARIANT_DMMA, 6, D, Q, NC, DmmaBody<D, Q, NC, 1, 128>, true, true>());
   out.push_back(entry<FK_VARIANT_DMMA, 7, D, Q, NC, DmmaBody<D, Q, NC, 1, 256>, true, true>());
   out.push_back(entry<FK_VARIANT_DMMA, 8, D, Q, NC, DmmaBody<D, Q, NC, E1, 256>, true, true>());
+  // cfgs 12-14: even-odd FMA stages A, B, D, E with stage C on DMMA
+  // (pa_eo_dmmac.cuh; d, q <= 8): E2 / E1 array-map geometries and the
+  // closed-form single-X precomputed-gather geometry of eo33
+  if constexpr (D <= 8 && Q <= 8) {
+    constexpr int E0c = base_E(Q);
+    constexpr int E1c = E0c / 2 > 0 ? E0c / 2 : 1;
+    constexpr int E2c = E0c / 4 > 0 ? E0c / 4 : 1;
+    using HC2 = EoDmmaCBody<D, Q, NC, E2c, round32(E2c * Q * Q),
+                            EoLayTuned<D, Q, NC, E2c, round32(E2c * Q * Q), false>, false>;
+    using HC1 = EoDmmaCBody<D, Q, NC, E1c, round32(E1c * Q * Q),
+                            EoLayTuned<D, Q, NC, E1c, round32(E1c * Q * Q), false>, false>;
+    using HC2s = EoDmmaCBody<D, Q, NC, E2c, round32(E2c * Q * Q),
+                             EoLayTuned<D, Q, NC, E2c, round32(E2c * Q * Q), false>, true, false>;
+    out.push_back(entry<FK_VARIANT_DMMA, 12, D, Q, NC, HC2, true>());
+    out.push_back(entry<FK_VARIANT_DMMA, 13, D, Q, NC, HC1, true>());
+    out.push_back(entry<FK_VARIANT_DMMA, 14, D, Q, NC, HC2s, true, false, false, 1, true, true>());
+  }
   // cfgs 9-11: one warp per element, stages chained in registers (d, q <= 8)
   if constexpr (D <= 8 && Q <= 8) {
     out.push_back(warp_dmma_entry<D, Q, NC, 4>(9));

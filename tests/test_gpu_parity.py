@@ -117,7 +117,7 @@ def test_apply_matches_oracle_all_orders(variant, kind, p, qoff):
     assert normwise(y, P.apply(x)) <= PARITY_TOL
 
 
-LAUNCH_CONFIGS = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(12)]
+LAUNCH_CONFIGS = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(15)]
                   + [("eo", c) for c in range(36)] + [("mf", c) for c in range(11)])
 
 
