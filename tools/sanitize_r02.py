@@ -2,7 +2,7 @@
 the quadratic-form CG geometries (QF twins, PA and MF, p = 2..8), the
 deterministic colour mode (apply, diagonal, CG), the closed-form box
 diagonal, the paper-style map DMMA body (p = 3, cfgs 3-5) and the new DMMA
-geometries (cfgs 6-8), the block operator's absorbing faces / free surface /
+geometries (cfgs 6-8), the warp-per-element and hybrid bodies (cfgs 9-14), the block operator's absorbing faces / free surface /
 bottom load / forced RK4, and a single-rank P2P communicator (its exchange
 kernels early-return; the multi-rank protocol runs in the rank-process tests).
 
@@ -44,7 +44,7 @@ for kind in ("mass", "diffusion"):
     op = PAOperator(build_mesh(4, 3, 2), 5, kind=kind)
     finite(op.diagonal())
     op.close()
-for cfg in range(3, 9):
+for cfg in range(3, 15):
     for kind in ("mass", "diffusion"):
         for dirichlet in (False, True):
             op = PAOperator(build_mesh(3, 2, 3), 3, kind=kind, dirichlet=dirichlet)
