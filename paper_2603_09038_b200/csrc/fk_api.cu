@@ -63,13 +63,13 @@ int grid_for(int64_t n, int threads, int num_sms) {
 // the repeated A/Bs r01_ab_p4_cfg29_32.log and r01_ab_p4_cfg32_35.log (cfg 35:
 // four elements per CTA, W over T2, no shared rows, closed-form ids, one X
 // buffer, precomputed gather: +6% over cfg 32 over 1000 applies);
-// tools/auto_table.py.  Structured-id geometries (eo19-24, 29-35) fall back
+// tools/auto_table.py.  Structured-id geometries (eo19-24, 29-49) fall back
 // to cfg 0 when the caller passes its own gather map
 constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
 const int kAutoCfg3[9] = {0, 19, 35, 35, 35, 25, 14, 18, 23};  // every p by 200-apply A/B: r01_ab_orders_*.log
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg1[9] = {0, 24, 31, 31, 30, 35, 30, 23, 30};  // every p by 200-apply A/B: r01_ab_orders_*.log
+const int kAutoCfg1[9] = {0, 24, 31, 49, 40, 47, 47, 43, 45};  // p <= 2: r01_ab_orders_*.log; p >= 3: staged scatter, r02_ab_bp1_ys.log
 
 int auto_variant(int nc, int p, int q) {
   (void)q;

@@ -435,6 +435,54 @@ struct DfmaEoBody {
     }
   }
 
+  // DR (BP1, pa_pipe.cuh): stage C's PA data in registers, loaded from global
+  // at the start of the batch (latency behind stages A and B) instead of a
+  // bulk copy into shared memory — D's 2 x 8q^3 bytes of shared-memory
+  // traffic per element go away and the CTA needs 8Eq^3 bytes less
+  static constexpr int DR_NIT = (E * Q * Q + T - 1) / T;
+  struct DRegs {
+    double v[DR_NIT][Q];
+  };
+  __device__ __forceinline__ static void load_d(const double* __restrict__ db, int ne, DRegs& r) {
+    static_assert(NC == 1, "PA data in registers: one component (BP1)");
+    constexpr int N = E * Q * Q;
+#pragma unroll
+    for (int pass = 0; pass < DR_NIT; ++pass) {
+      const int t0 = threadIdx.x + pass * T;
+      int e, a, b;
+      line_map<LP::MC, E, Q, Q>(t0 < N ? t0 : 0, e, a, b);
+      const bool act = t0 < N && e < ne;
+      const double* pe = db + (act ? e : 0) * G::PS + a + Q * b;
+#pragma unroll
+      for (int c = 0; c < Q; ++c) r.v[pass][c] = act ? __ldcs(pe + c * Q * Q) : 0.0;
+    }
+  }
+  __device__ __forceinline__ static void stage_c_dr(const Tab& tb, int it, const double* s0, const DRegs& r,
+                                                    double* sw, int ne, double*) {
+    const double* tab = tb.t[PP ? (it & 1) : 0];
+    constexpr int N = E * Q * Q;
+#pragma unroll
+    for (int pass = 0; pass < DR_NIT; ++pass) {
+      const int t0 = threadIdx.x + pass * T;
+      int e, a, b;
+      line_map<LP::MC, E, Q, Q>(t0 < N ? t0 : 0, e, a, b);
+      const bool act = t0 < N && e < ne;
+      if (!act) e = 0;
+      double tin[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) tin[k] = s0[LT2::at(e, 0, a, b, k)];
+      if constexpr (IP) __syncthreads();
+      if (!act) continue;
+      double g[Q], w[D];
+      contract_eo<D, Q, +1>(tab + Tab::TB, tin, g);
+#pragma unroll
+      for (int c = 0; c < Q; ++c) g[c] *= r.v[pass][c];
+      contract_eo<Q, D, +1>(tab + Tab::TBT, g, w);
+#pragma unroll
+      for (int k = 0; k < D; ++k) sw[LW::at(e, 0, a, b, k)] = w[k];
+    }
+  }
+
   // W (a, b, k) -> R (a, j, k): thread per line (a, k)
   __device__ __forceinline__ static void stage_d(const Tab& tb, int it, const double* sw, double* sr,
                                                  int ne, double*) {
@@ -485,6 +533,34 @@ struct DfmaEoBody {
         contract_eo<Q, D, +1>(tab + Tab::TBT, rv, out);
 #pragma unroll
         for (int i = 0; i < D; ++i) atomicAdd(y + g0 + i, out[i]);
+      }
+    });
+  }
+
+  // staged scatter (pa_pipe.cuh YS): stage E's line outputs go to the dead W
+  // region in the X-buffer layout; the pipeline then issues the RED.F64s in
+  // the gather's thread -> node order (consecutive lanes on consecutive nodes
+  // of a row: ~3x fewer L2 sectors per warp-wide RED than one line per lane)
+  static constexpr bool YS_FITS = XS <= (IP ? P0 : P1);
+  __device__ __forceinline__ static void stage_e_stage(const Tab& tb, int it, const double* sr, double* yb,
+                                                       int ne, double*) {
+    const double* tab = tb.t[PP ? (it & 1) : 0];
+    lines<LP::ME, D, D>(ne, [&](int e, int j, int k) {
+      double rv[Q], out[D];
+#pragma unroll
+      for (int a = 0; a < Q; ++a) rv[a] = sr[LR::at(e, 0, a, j, k)];
+      if constexpr (NC == 3) {
+        double o2[D];
+        contract_eo<Q, D, -1>(tab + Tab::TGT, rv, out);  // G^T rG
+#pragma unroll
+        for (int a = 0; a < Q; ++a) rv[a] = sr[LR::at(e, 1, a, j, k)];
+        contract_eo<Q, D, +1>(tab + Tab::TBT, rv, o2);  // B^T rB
+#pragma unroll
+        for (int i = 0; i < D; ++i) yb[LX::at(e, 0, i, j, k)] = out[i] + o2[i];
+      } else {
+        contract_eo<Q, D, +1>(tab + Tab::TBT, rv, out);
+#pragma unroll
+        for (int i = 0; i < D; ++i) yb[LX::at(e, 0, i, j, k)] = out[i];
       }
     });
   }

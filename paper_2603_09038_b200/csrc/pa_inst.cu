@@ -48,13 +48,13 @@ StructIds struct_ids(const OpView& v) {
 }
 
 template <int D, int Q, int NC, class Body, bool PERSIST, bool DG, bool MF = false, int GM = 0,
-          bool SX = false, bool XP = false, bool QF = false>
+          bool SX = false, bool XP = false, bool QF = false, bool YS = false, bool DR = false>
 void launch_pipe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
   typename Body::Tab tb;
   Body::fill(tb, v.B, v.G);
   if constexpr (MF) Body::fill_mf(tb, v.w, v.detj, v.jinv);
   const StructIds sid = struct_ids(v);
-  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, QF>
+  pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, QF, YS, DR>
       <<<blocks, Body::T, PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES, s>>>(
           tb, x, y, v.gids, v.pa, v.ebits, v.nel, sid);
 }
@@ -113,7 +113,8 @@ constexpr bool qf_cfg(int variant, int cfg) {
 }
 
 template <int V, int CFG, int D, int Q, int NC, class Body, bool PERSIST = true, bool DG = false,
-          bool MF = false, int GM = 0, bool SX = false, bool XP = false>
+          bool MF = false, int GM = 0, bool SX = false, bool XP = false, bool YS = false,
+          bool DR = false>
 KernelEntry entry() {
   constexpr int variant = V, cfg = CFG;
   KernelEntry k;
@@ -126,14 +127,14 @@ KernelEntry entry() {
   k.T = Body::T;
   k.persist = PERSIST;
   k.structured = GM == 1;
-  if constexpr (NC == 3 && Q == D + 1 && PERSIST && HasQf<Body>::value && qf_cfg(V, CFG))
+  if constexpr (NC == 3 && Q == D + 1 && PERSIST && !DR && HasQf<Body>::value && qf_cfg(V, CFG))
   {
-    k.launch_qf = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, true>;
-    k.func_qf = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, true>);
+    k.launch_qf = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, true, YS, DR>;
+    k.func_qf = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, true, YS, DR>);
   }
   k.smem = PipeSmem<D, Q, NC, Body, DG || MF, GM, SX>::BYTES;
-  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>);
-  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP>;
+  k.func = reinterpret_cast<const void*>(&pa_pipe_kernel<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, false, YS, DR>);
+  k.launch = &launch_pipe<D, Q, NC, Body, PERSIST, DG, MF, GM, SX, XP, false, YS, DR>;
   k.diag = &launch_diag<D, Q, NC>;
   k.diag_func = reinterpret_cast<const void*>(&diagonal_kernel<D, Q, NC>);
   return k;
@@ -249,6 +250,57 @@ void add_all(std::vector<KernelEntry>& out) {
   out.push_back(entry<FK_VARIANT_EO, 33, D, Q, NC, TunedEo<D, Q, NC, E2, false, true, false>, true, false, false, 1, true, true>());
   out.push_back(entry<FK_VARIANT_EO, 34, D, Q, NC, TunedEo<D, Q, NC, E2, true, true, false>, true, false, false, 1, false, true>());
   out.push_back(entry<FK_VARIANT_EO, 35, D, Q, NC, TunedEo<D, Q, NC, E1, true, true, false>, true, false, false, 1, true, true>());
+  // cfgs 36-39: one-warp CTAs (T = 32): a CTA barrier is one warp's, up to 32
+  // CTAs per SM hide each other's latency; lines over E = 1 / 2 / 4 elements
+  // in several passes (layouts searched for T = 32, pa_eo_layouts.cuh);
+  // closed-form ids, single X, precomputed gather as cfg 30
+  if constexpr (Q == D + 1) {
+    using W1 = DfmaEoBody<D, Q, NC, 1, 32, EoLayTuned<D, Q, NC, 1, 32, false>, false>;
+    out.push_back(entry<FK_VARIANT_EO, 36, D, Q, NC, W1, true, false, false, 1, true, true>());
+    if constexpr (NC == 1) {
+      using W2 = DfmaEoBody<D, Q, NC, 2, 32, EoLayTuned<D, Q, NC, 2, 32, false>, false>;
+      using W4 = DfmaEoBody<D, Q, NC, 4, 32, EoLayTuned<D, Q, NC, 4, 32, false>, false>;
+      out.push_back(entry<FK_VARIANT_EO, 37, D, Q, NC, W2, true, false, false, 1, true, true>());
+      out.push_back(entry<FK_VARIANT_EO, 38, D, Q, NC, W4, true, false, false, 1, true, true>());
+      // 39: E = 2 with two X buffers (next gather issued before stage A)
+      out.push_back(entry<FK_VARIANT_EO, 39, D, Q, NC, W2, true, false, false, 1, false, true>());
+    }
+  }
+  // cfgs 40-45: staged scatter (YS) twins of cfgs 30, 35, 23, 24, 31, 29 —
+  // stage E's outputs through shared memory so the RED.F64s go out in node
+  // order (tools/scatter_bench.cu: 300 vs 154 G RED/s at p = 4); geometries
+  // whose X layout does not fit in the W region are not compiled
+  if constexpr (Q == D + 1) {
+    using Y30 = TunedEo<D, Q, NC, E1, false, false>;
+    using Y35 = TunedEo<D, Q, NC, E1, true, true, false>;
+    using Y24 = TunedEo<D, Q, NC, E0, true, false>;
+    using Y29 = TunedEo<D, Q, NC, E2, true, true>;
+    if constexpr (Y30::YS_FITS) {
+      out.push_back(entry<FK_VARIANT_EO, 40, D, Q, NC, Y30, true, false, false, 1, true, true, true>());
+      out.push_back(entry<FK_VARIANT_EO, 42, D, Q, NC, Y30, true, false, false, 1, true, false, true>());
+    }
+    if constexpr (Y35::YS_FITS)
+      out.push_back(entry<FK_VARIANT_EO, 41, D, Q, NC, Y35, true, false, false, 1, true, true, true>());
+    if constexpr (Y24::YS_FITS) {
+      out.push_back(entry<FK_VARIANT_EO, 43, D, Q, NC, Y24, true, false, false, 1, true, false, true>());
+      out.push_back(entry<FK_VARIANT_EO, 44, D, Q, NC, Y24, true, false, false, 1, true, true, true>());
+    }
+    if constexpr (Y29::YS_FITS)
+      out.push_back(entry<FK_VARIANT_EO, 45, D, Q, NC, Y29, true, false, false, 1, true, true, true>());
+    // cfgs 46-49 (BP1): cfgs 40, 41, 43, 44 with stage C's PA data loaded
+    // into registers at the start of the batch (DR) instead of bulk-copied to
+    // shared memory
+    if constexpr (NC == 1) {
+      if constexpr (Y30::YS_FITS)
+        out.push_back(entry<FK_VARIANT_EO, 46, D, Q, NC, Y30, true, true, false, 1, true, true, true, true>());
+      if constexpr (Y35::YS_FITS)
+        out.push_back(entry<FK_VARIANT_EO, 47, D, Q, NC, Y35, true, true, false, 1, true, true, true, true>());
+      if constexpr (Y24::YS_FITS) {
+        out.push_back(entry<FK_VARIANT_EO, 48, D, Q, NC, Y24, true, true, false, 1, true, false, true, true>());
+        out.push_back(entry<FK_VARIANT_EO, 49, D, Q, NC, Y24, true, true, false, 1, true, true, true, true>());
+      }
+    }
+  }
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;
   using M1 = TunedEo<D, Q, NC, E1, false, true>;

@@ -65,6 +65,16 @@ struct StructIds {
   double* qf;  // non-null: CTA b writes its share of sum_e x_e^T A_e x_e to qf[b]
 };
 
+// register PA data of a DR launch (pa_dfma_eo.cuh DfmaEoBody::DRegs)
+template <class B, bool DR>
+struct DRegsOf {
+  struct type {};
+};
+template <class B>
+struct DRegsOf<B, true> {
+  using type = typename B::DRegs;
+};
+
 // bodies whose stage C can accumulate the element quadratic form (QF_OK)
 template <class B, class = void>
 struct HasQf {
@@ -113,7 +123,7 @@ struct PipeSmem {
 // no id array traffic, one int per element per slot.  SX: a single X buffer;
 // the next batch's gather is issued after stage A has consumed the current one.
 template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false, bool MF = false, int GM = 0,
-          bool SX = false, bool XP = false, bool QF = false>
+          bool SX = false, bool XP = false, bool QF = false, bool YS = false, bool DR = false>
 __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ typename Body::Tab tb,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
@@ -265,6 +275,25 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     }
     cp_async_commit();
   };
+  // staged scatter (YS): y[gid] += yb[X offset] in issue_x's thread -> node map
+  auto scatter_y = [&](int gslot, int ne, const double* yb) {
+    if constexpr (XPRE) {
+#pragma unroll
+      for (int r = 0; r < NXT; ++r) {
+        const int e = x_el[r] >> 16;
+        if (e < ne) {
+          const int g = GM == 1 ? gs[gslot * E + e] + x_rel[r] : gs[gslot * E * G::GS + x_rel[r]];
+          atomicAdd(y + g, yb[x_off[r]]);
+        }
+      }
+    } else {
+      for (int t = threadIdx.x; t < E * D3; t += T) {
+        int e, l;
+        XA::map(t, e, l);
+        if (e < ne) atomicAdd(y + gid_of(gslot, e, l), yb[XA::off(e, l)]);
+      }
+    }
+  };
   auto finish_x = [&](int gslot, int ne, double* xsrc) {
     cp_async_wait_all();
     if (dirichlet) {
@@ -320,6 +349,9 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     double* xnext = SX ? xb : xb + ((it + 1) & 1) * E * XS;
     const int e0 = b * E, ne = min(E, nel - e0);
     const int nb = b + stride, nb2 = nb + stride;
+    // DR: this batch's PA data into registers now, consumed in stage C
+    [[maybe_unused]] typename DRegsOf<Body, DR>::type dreg;
+    if constexpr (DR) Body::load_d(pa + (size_t)e0 * G::PS, ne, dreg);
     finish_x(gslot, ne, xcur);
     __syncthreads();
     if (nb < nbatch) {
@@ -355,6 +387,8 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
       }
     } else if constexpr (MF) {
       Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex);
+    } else if constexpr (DR) {
+      Body::stage_c_dr(tb, it, s0, dreg, sw, ne, ex);
     } else if constexpr (DG) {
       Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex);
     } else {
@@ -369,7 +403,15 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     }
     Body::stage_d(tb, it, sw, sr, ne, ex);
     __syncthreads();
-    if constexpr (GM == 1) {
+    if constexpr (YS) {
+      // staged scatter: outputs into the dead W region (X layout), then the
+      // RED.F64s in the gather's thread -> node order.  The next writer of sw
+      // (stage A or B of the next batch) runs after that batch's first barrier.
+      static_assert(Body::YS_FITS, "staged scatter needs the X layout to fit in the W region");
+      Body::stage_e_stage(tb, it, sr, sw, ne, ex);
+      __syncthreads();
+      scatter_y(gslot, ne, sw);
+    } else if constexpr (GM == 1) {
       Body::stage_e_ids(
           tb, it, sr, [&](int e, int j, int k) { return gs[gslot * E + e] + sid.npx * (j + sid.npy * k); },
           y, ne, ex);

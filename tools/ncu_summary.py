@@ -24,6 +24,9 @@ WANT = [
     "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum", "lts__t_sector_hit_rate.pct",
     "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__cycles_elapsed.avg.per_second",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_requests_op_red.sum",
+    "lts__t_sectors.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+    "lts__d_sectors.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
