@@ -145,6 +145,14 @@ struct MixLayout {
   __device__ __forceinline__ static int ru(int e, int r, int a, int j, int k) {
     return e * R0S + OFF_RU + w<typename St::RU>(r, a, j, k);
   }
+  // staged outputs (YS), region 1 after stage D: p block (X-buffer layout)
+  // then the three u blocks, node order within each
+  static constexpr int YUO = XPS;
+  static_assert(YUO + 3 * XUC <= R1S, "staged outputs must fit in region 1");
+  __device__ __forceinline__ static int yp(int e, int i, int j, int k) { return e * R1S + i + LSP * (j + DP * k); }
+  __device__ __forceinline__ static int yu(int e, int r, int i, int j, int k) {
+    return e * R1S + YUO + r * XUC + i + LSU * (j + DU * k);
+  }
   // global: PA data 9 components per point, int32 gather ids
   static constexpr int PS = pa_pad(((9 * Q3 + 1) / 2) * 2, Q);
   static constexpr int GS = ((DP3 + 3) / 4) * 4;
@@ -177,7 +185,13 @@ struct MixArgs {
 // MF (FusedMF strategy, operator.py:280-286): no dmat traffic — stage C
 // recomputes the diagonal w|J|J^-1 of the axis-aligned box from the 1D weights
 // in the PA setup's operation order.
-template <int DP, int DU, int Q, int E, int T, bool TAU, bool VB, bool MF = false>
+//
+// YS (staged outputs): stage E writes both blocks' outputs to region 1 (T1/W,
+// dead after stage D) in node order; after one barrier out_u is stored
+// contiguously across the batch's elements and out_p's RED.F64s go out in
+// node order — instead of one x-line per lane, where every warp-wide store /
+// RED touches ~32 rows (tools/scatter_bench.cu).
+template <int DP, int DU, int Q, int E, int T, bool TAU, bool VB, bool MF = false, bool YS = false>
 __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ MixTables<DP, DU, Q> tb,
                                                      const MixArgs arg) {
   using L = MixLayout<DP, DU, Q>;
@@ -461,6 +475,47 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
     // ---- stage E: x^T, outputs
     const int* g = gs + gslot * E * GS;
     constexpr int NEU = TAU ? 3 * DU * DU : 0, NEP = VB ? DP * DP : 0;
+    if constexpr (YS) {
+      lines(ne, NEU, NEP, [&](int e, int l) {
+        if (TAU && l < NEU) {
+          const int r = l / (DU * DU), jk = l - r * (DU * DU), j = jk % DU, k = jk / DU;
+          double v[Q], o[DU];
+#pragma unroll
+          for (int a = 0; a < Q; ++a) v[a] = s0[L::ru(e, r, a, j, k)];
+          contract_eo<Q, DU, +1>(tab + Tb::TBUT, v, o);
+#pragma unroll
+          for (int i = 0; i < DU; ++i) s1[L::yu(e, r, i, j, k)] = o[i];
+        } else if (VB) {
+          const int m = l - NEU, j = m % DP, k = m / DP;
+          double v[Q], o[DP], o2[DP];
+#pragma unroll
+          for (int a = 0; a < Q; ++a) v[a] = s0[L::rp(e, 0, a, j, k)];
+          contract_eo<Q, DP, -1>(tab + Tb::TGPT, v, o);  // G^T rG
+#pragma unroll
+          for (int a = 0; a < Q; ++a) v[a] = s0[L::rp(e, 1, a, j, k)];
+          contract_eo<Q, DP, +1>(tab + Tb::TBPT, v, o2);  // B^T rB
+#pragma unroll
+          for (int i = 0; i < DP; ++i) s1[L::yp(e, i, j, k)] = o[i] + o2[i];
+        }
+      });
+      __syncthreads();
+      if constexpr (TAU) {  // (3, nel, DU^3): contiguous over the batch for each r
+        for (int t = threadIdx.x; t < 3 * E * DU3; t += T) {
+          const int r = t / (E * DU3), m = t - r * (E * DU3), e = m / DU3, l = m - e * DU3;
+          if (e < ne)
+            arg.out_u[((size_t)r * nel + e0 + e) * DU3 + l] =
+                arg.su * s1[L::yu(e, r, l % DU, (l / DU) % DU, l / (DU * DU))];
+        }
+      }
+      if constexpr (VB) {
+        for (int t = threadIdx.x; t < E * DP3; t += T) {
+          const int e = t / DP3, l = t - e * DP3;
+          if (e < ne)
+            atomicAdd(arg.out_p + g[e * GS + l], arg.sp * s1[L::yp(e, l % DP, (l / DP) % DP, l / (DP * DP))]);
+        }
+      }
+      continue;  // region 1 is next written by the next batch's stage A, after its first barrier
+    }
     lines(ne, NEU, NEP, [&](int e, int l) {
       if (TAU && l < NEU) {
         const int r = l / (DU * DU), jk = l - r * (DU * DU), j = jk % DU, k = jk / DU;
