@@ -223,6 +223,16 @@ struct EoLayDefault {
   using R = BufLay<RST, D * D * LQ, 1, LQ, D * LQ>;
 };
 
+// layout policies of bodies that replace stages B-D (pa_eo_bcd.cuh: NO_C)
+template <class LP, class = void>
+struct LayNoC {
+  static constexpr bool value = false;
+};
+template <class LP>
+struct LayNoC<LP, decltype((void)LP::NO_C)> {
+  static constexpr bool value = LP::NO_C;
+};
+
 // Even-odd FP64-FMA body over layout policy LP (EoLayDefault or a searched
 // layout).  W_OVER_T2 (in place): stage C reads its T2 line into registers,
 // the CTA syncs, and W overwrites T2 in region 0; R then lives in region 1 —
@@ -267,7 +277,7 @@ struct DfmaEoBody {
       e = t - l * E;
     }
   }
-  static_assert(!IP || E * Q * Q <= T, "in-place stage C needs one pass over its lines");
+  static_assert(!IP || E * Q * Q <= T || LayNoC<LP>::value, "in-place stage C needs one pass over its lines");
 
   static void fill(Tab& tb, const double* B, const double* Gr) {
     double Bt[Q * D], Gt[Q * D];

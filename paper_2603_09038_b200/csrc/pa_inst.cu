@@ -16,6 +16,7 @@
 #include "pa_dmma.cuh"
 #include "pa_dmma_map.cuh"
 #include "pa_dmma_warp.cuh"
+#include "pa_eo_bcd.cuh"
 #include "pa_eo_dmmac.cuh"
 #include "pa_pipe.cuh"
 
@@ -300,6 +301,19 @@ void add_all(std::vector<KernelEntry>& out) {
         out.push_back(entry<FK_VARIANT_EO, 49, D, Q, NC, Y24, true, true, false, 1, true, true, true, true>());
       }
     }
+  }
+  // cfgs 50-53 (BP1): stages B, C, D fused in registers (pa_eo_bcd.cuh), E =
+  // 4 / 8 / 16 / 2 elements per CTA, one thread per (element, a) slab; staged
+  // scatter, closed-form ids, single X, precomputed gather
+  if constexpr (NC == 1 && Q == D + 1) {
+    using B4 = EoBcdBody<D, Q, 4, round32(4 * Q)>;
+    using B8 = EoBcdBody<D, Q, 8, round32(8 * Q)>;
+    using B16 = EoBcdBody<D, Q, 16, round32(16 * Q)>;
+    using B2 = EoBcdBody<D, Q, 2, round32(2 * Q)>;
+    out.push_back(entry<FK_VARIANT_EO, 50, D, Q, NC, B4, true, false, false, 1, true, true, true>());
+    out.push_back(entry<FK_VARIANT_EO, 51, D, Q, NC, B8, true, false, false, 1, true, true, true>());
+    out.push_back(entry<FK_VARIANT_EO, 52, D, Q, NC, B16, true, false, false, 1, true, true, true>());
+    out.push_back(entry<FK_VARIANT_EO, 53, D, Q, NC, B2, true, false, false, 1, true, true, true>());
   }
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;

@@ -75,6 +75,17 @@ struct DRegsOf<B, true> {
   using type = typename B::DRegs;
 };
 
+// bodies that run stages B, C and D as one register-resident stage
+// (pa_eo_bcd.cuh FUSED_BCD): A, stage_bcd, E — three CTA barriers per batch
+template <class B, class = void>
+struct HasBcd {
+  static constexpr bool value = false;
+};
+template <class B>
+struct HasBcd<B, decltype((void)B::FUSED_BCD)> {
+  static constexpr bool value = B::FUSED_BCD;
+};
+
 // bodies whose stage C can accumulate the element quadratic form (QF_OK)
 template <class B, class = void>
 struct HasQf {
@@ -373,6 +384,18 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
         issue_x(nb, (it + 1) % NG, xnext);
       }
     }
+    if constexpr (HasBcd<Body>::value) {
+      // stages B, C, D in registers (pa_eo_bcd.cuh): T1 -> R in place in region 1
+      static_assert(!DG && !MF && !DR && !QF, "fused B-C-D reads the PA data from shared memory");
+      mbar_wait(bar_d, ph_d);
+      ph_d ^= 1u;
+      Body::stage_bcd(tb, s1, db, ne);
+      __syncthreads();
+      if (nb < nbatch && threadIdx.x == 0) {
+        fence_proxy_async();
+        issue_d(nb);
+      }
+    } else {
     Body::stage_b(tb, it, s1, s0, ne, ex);
     __syncthreads();
     if constexpr (QF && HasQf<Body>::value) {
@@ -403,6 +426,7 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     }
     Body::stage_d(tb, it, sw, sr, ne, ex);
     __syncthreads();
+    }
     if constexpr (YS) {
       // staged scatter: outputs into the dead W region (X layout), then the
       // RED.F64s in the gather's thread -> node order.  The next writer of sw
