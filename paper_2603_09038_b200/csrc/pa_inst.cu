@@ -17,6 +17,7 @@
 #include "pa_dmma_map.cuh"
 #include "pa_dmma_warp.cuh"
 #include "pa_eo_bcd.cuh"
+#include "pa_eo_ds.cuh"
 #include "pa_eo_dmmac.cuh"
 #include "pa_pipe.cuh"
 
@@ -314,6 +315,20 @@ void add_all(std::vector<KernelEntry>& out) {
     out.push_back(entry<FK_VARIANT_EO, 51, D, Q, NC, B8, true, false, false, 1, true, true, true>());
     out.push_back(entry<FK_VARIANT_EO, 52, D, Q, NC, B16, true, false, false, 1, true, true, true>());
     out.push_back(entry<FK_VARIANT_EO, 53, D, Q, NC, B2, true, false, false, 1, true, true, true>());
+  }
+  // cfgs 54-57 (BP3, p >= 4): PA data streamed through a two-slot ring of
+  // c-plane pairs (pa_eo_ds.cuh) instead of the batch's whole D in shared
+  // memory: 54 / 55 one element per CTA (W over T1 / in place), 56 two
+  // elements, 57 = 54 without the precomputed gather
+  if constexpr (NC == 3 && Q == D + 1 && D >= 5) {
+    constexpr int T1e = round32(Q * Q), T2e = round32(2 * Q * Q);
+    using S54 = EoDsBody<D, Q, NC, 1, T1e, EoLayTuned<D, Q, NC, 1, T1e, false>, false>;
+    using S55 = EoDsBody<D, Q, NC, 1, T1e, EoLayTuned<D, Q, NC, 1, T1e, true>, false>;
+    using S56 = EoDsBody<D, Q, NC, 2, T2e, EoLayTuned<D, Q, NC, 2, T2e, false>, false>;
+    out.push_back(entry<FK_VARIANT_EO, 54, D, Q, NC, S54, true, false, false, 1, true, true>());
+    out.push_back(entry<FK_VARIANT_EO, 55, D, Q, NC, S55, true, false, false, 1, true, true>());
+    out.push_back(entry<FK_VARIANT_EO, 56, D, Q, NC, S56, true, false, false, 1, true, true>());
+    out.push_back(entry<FK_VARIANT_EO, 57, D, Q, NC, S54, true, false, false, 1, true, false>());
   }
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;

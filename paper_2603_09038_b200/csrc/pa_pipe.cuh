@@ -86,6 +86,27 @@ struct HasBcd<B, decltype((void)B::FUSED_BCD)> {
   static constexpr bool value = B::FUSED_BCD;
 };
 
+// bodies that stream the PA data through a two-slot ring of c-plane pairs
+// (pa_eo_ds.cuh D_STREAM)
+template <class B, class = void>
+struct HasDs {
+  static constexpr bool value = false;
+};
+template <class B>
+struct HasDs<B, decltype((void)B::D_STREAM)> {
+  static constexpr bool value = B::D_STREAM;
+};
+// shared-memory bytes of the PA data region: the batch's D (bulk copy), none
+// (D from global / matrix-free), or two ring barriers + two pair slots
+template <class B, bool NOD, bool DS = HasDs<B>::value>
+struct DRegion {
+  static constexpr size_t bytes(size_t batch) { return NOD ? 0ull : batch; }
+};
+template <class B, bool NOD>
+struct DRegion<B, NOD, true> {
+  static constexpr size_t bytes(size_t) { return 16ull + 16ull * B::SLOT; }
+};
+
 // bodies whose stage C can accumulate the element quadratic form (QF_OK)
 template <class B, class = void>
 struct HasQf {
@@ -116,7 +137,7 @@ struct PipeSmem {
   // byte offsets (16-byte aligned where bulk copies land)
   static constexpr size_t OFF_BAR = 0;                                 // 4 mbarriers
   static constexpr size_t OFF_DB = 32;                                 // PA data
-  static constexpr size_t OFF_GS = OFF_DB + (DG ? 0ull : 8ull * E * G::PS);  // NG gid slots
+  static constexpr size_t OFF_GS = OFF_DB + DRegion<Body, DG>::bytes(8ull * E * G::PS);  // NG gid slots
   static constexpr size_t OFF_MS = OFF_GS + (4ull * NG * E * GSS + 15) / 16 * 16;  // NG bit slots
   static constexpr size_t OFF_S0 = OFF_MS + 4ull * NG * E * G::MS;
   static constexpr size_t OFF_S1 = OFF_S0 + 8ull * E * Body::P0;
@@ -163,10 +184,17 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
   double* sw = Body::IP ? s0 : s1;
   double* sr = Body::IP ? s1 : s0;
 
+  constexpr bool DS = HasDs<Body>::value;
+  uint64_t* bar_r = reinterpret_cast<uint64_t*>(smem_raw + S::OFF_DB);   // DS: ring barriers
+  double* ring = reinterpret_cast<double*>(smem_raw + S::OFF_DB + 16);  // DS: two pair slots
   const int nbatch = (nel + E - 1) / E;
   if ((int)blockIdx.x >= nbatch) return;
   const bool dirichlet = ebits != nullptr;
   if (threadIdx.x == 0) {
+    if constexpr (DS) {
+      mbar_init(bar_r, 1);
+      mbar_init(bar_r + 1, 1);
+    }
     mbar_init(bar_d, 1);
 #pragma unroll
     for (int s = 0; s < NG; ++s) mbar_init(bar_g + s, 1);
@@ -221,7 +249,7 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     }
   };
   auto issue_d = [&](int b) {
-    if constexpr (MF) return;
+    if constexpr (MF || DS) return;
     const int e0 = b * E, ne = min(E, nel - e0);
     const uint32_t bytes = 8u * ne * G::PS;
     if constexpr (DG) {
@@ -233,6 +261,26 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
 #else
       bulk_g2s_hint(db, pa + (size_t)e0 * G::PS, bytes, bar_d, l2_policy_evict_first());
 #endif
+    }
+  };
+  // DS (thread 0): the plane windows of pair sp of batch b into ring slot `slot`
+  [[maybe_unused]] auto issue_pair = [&](int b, int sp, int slot) {
+    if constexpr (DS) {
+      const int e0 = b * E, ne = min(E, nel - e0);
+      const int c0 = sp, c1 = Q - 1 - sp, nh = c0 != c1 ? 2 : 1;
+      uint32_t bytes = 0;
+      for (int m = 0; m < Body::NPA; ++m)
+        for (int h = 0; h < nh; ++h) bytes += 8u * Body::win_len(m, h ? c1 : c0);
+      mbar_expect_tx(bar_r + slot, bytes * (uint32_t)ne);
+      const double* pb = pa + (size_t)e0 * G::PS;
+      double* dst = ring + slot * Body::SLOT;
+      for (int e = 0; e < ne; ++e)
+        for (int m = 0; m < Body::NPA; ++m)
+          for (int h = 0; h < nh; ++h) {
+            const int c = h ? c1 : c0;
+            bulk_g2s(dst + Body::slot_at(e, m, h), pb + Body::win_off(e, m, c), 8u * Body::win_len(m, c),
+                     bar_r + slot);
+          }
     }
   };
   // XP: this thread's gather slots are the same in every batch, so their
@@ -340,6 +388,12 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
     issue_g(blockIdx.x, 0);
     if (blockIdx.x + stride < nbatch) issue_g(blockIdx.x + stride, 1);
     issue_d(blockIdx.x);
+    if constexpr (DS) {  // pairs 0 and 1 of the global pair sequence (it * NP + pair)
+      for (int g2 = 0; g2 < 2; ++g2) {
+        const int bb = (int)blockIdx.x + (g2 / Body::NP) * stride;
+        if (bb < nbatch) issue_pair(bb, g2 % Body::NP, g2);
+      }
+    }
   }
   if constexpr (GM == 1) {  // base ids of the first two batches
     fill_base(blockIdx.x, 0);
@@ -408,6 +462,26 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
         ph_d ^= 1u;
         Body::stage_c(tb, it, s0, db, sw, ne, ex, qptr);
       }
+    } else if constexpr (DS) {
+      static_assert(!DG && !MF && !DR, "streamed PA data comes from the ring");
+      Body::stage_c_ds(
+          tb, it, s0, sw, ne,
+          [&](int sp) -> const double* {
+            const int gp = it * Body::NP + sp, slot = gp & 1;
+            mbar_wait(bar_r + slot, (uint32_t)((gp >> 1) & 1));
+            return ring + slot * Body::SLOT;
+          },
+          [&](int sp) {
+            __syncthreads();  // every thread is done with this pair's slot
+            if (threadIdx.x == 0) {
+              const int gp = it * Body::NP + sp + 2;
+              const int bb = b + (gp / Body::NP - it) * stride;
+              if (bb < nbatch) {
+                fence_proxy_async();
+                issue_pair(bb, gp % Body::NP, gp & 1);
+              }
+            }
+          });
     } else if constexpr (MF) {
       Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex);
     } else if constexpr (DR) {
