@@ -450,56 +450,56 @@ __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant_
         issue_d(nb);
       }
     } else {
-    Body::stage_b(tb, it, s1, s0, ne, ex);
-    __syncthreads();
-    if constexpr (QF && HasQf<Body>::value) {
-      if constexpr (MF) {
-        Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex, qptr);
+      Body::stage_b(tb, it, s1, s0, ne, ex);
+      __syncthreads();
+      if constexpr (QF && HasQf<Body>::value) {
+        if constexpr (MF) {
+          Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex, qptr);
+        } else if constexpr (DG) {
+          Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex, qptr);
+        } else {
+          mbar_wait(bar_d, ph_d);
+          ph_d ^= 1u;
+          Body::stage_c(tb, it, s0, db, sw, ne, ex, qptr);
+        }
+      } else if constexpr (DS) {
+        static_assert(!DG && !MF && !DR, "streamed PA data comes from the ring");
+        Body::stage_c_ds(
+            tb, it, s0, sw, ne,
+            [&](int sp) -> const double* {
+              const int gp = it * Body::NP + sp, slot = gp & 1;
+              mbar_wait(bar_r + slot, (uint32_t)((gp >> 1) & 1));
+              return ring + slot * Body::SLOT;
+            },
+            [&](int sp) {
+              __syncthreads();  // every thread is done with this pair's slot
+              if (threadIdx.x == 0) {
+                const int gp = it * Body::NP + sp + 2;
+                const int bb = b + (gp / Body::NP - it) * stride;
+                if (bb < nbatch) {
+                  fence_proxy_async();
+                  issue_pair(bb, gp % Body::NP, gp & 1);
+                }
+              }
+            });
+      } else if constexpr (MF) {
+        Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex);
+      } else if constexpr (DR) {
+        Body::stage_c_dr(tb, it, s0, dreg, sw, ne, ex);
       } else if constexpr (DG) {
-        Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex, qptr);
+        Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex);
       } else {
         mbar_wait(bar_d, ph_d);
         ph_d ^= 1u;
-        Body::stage_c(tb, it, s0, db, sw, ne, ex, qptr);
+        Body::stage_c(tb, it, s0, db, sw, ne, ex);
       }
-    } else if constexpr (DS) {
-      static_assert(!DG && !MF && !DR, "streamed PA data comes from the ring");
-      Body::stage_c_ds(
-          tb, it, s0, sw, ne,
-          [&](int sp) -> const double* {
-            const int gp = it * Body::NP + sp, slot = gp & 1;
-            mbar_wait(bar_r + slot, (uint32_t)((gp >> 1) & 1));
-            return ring + slot * Body::SLOT;
-          },
-          [&](int sp) {
-            __syncthreads();  // every thread is done with this pair's slot
-            if (threadIdx.x == 0) {
-              const int gp = it * Body::NP + sp + 2;
-              const int bb = b + (gp / Body::NP - it) * stride;
-              if (bb < nbatch) {
-                fence_proxy_async();
-                issue_pair(bb, gp % Body::NP, gp & 1);
-              }
-            }
-          });
-    } else if constexpr (MF) {
-      Body::template stage_c<true>(tb, it, s0, nullptr, sw, ne, ex);
-    } else if constexpr (DR) {
-      Body::stage_c_dr(tb, it, s0, dreg, sw, ne, ex);
-    } else if constexpr (DG) {
-      Body::stage_c(tb, it, s0, pa + (size_t)e0 * G::PS, sw, ne, ex);
-    } else {
-      mbar_wait(bar_d, ph_d);
-      ph_d ^= 1u;
-      Body::stage_c(tb, it, s0, db, sw, ne, ex);
-    }
-    __syncthreads();
-    if (nb < nbatch && threadIdx.x == 0) {
-      fence_proxy_async();
-      issue_d(nb);
-    }
-    Body::stage_d(tb, it, sw, sr, ne, ex);
-    __syncthreads();
+      __syncthreads();
+      if (nb < nbatch && threadIdx.x == 0) {
+        fence_proxy_async();
+        issue_d(nb);
+      }
+      Body::stage_d(tb, it, sw, sr, ne, ex);
+      __syncthreads();
     }
     if constexpr (YS) {
       // staged scatter: outputs into the dead W region (X layout), then the
