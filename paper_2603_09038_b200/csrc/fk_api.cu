@@ -69,7 +69,7 @@ constexpr int D_ = FK_VARIANT_DFMA, O_ = FK_VARIANT_EO;
 const int kAutoVar3[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
 const int kAutoCfg3[9] = {0, 19, 35, 35, 35, 25, 14, 18, 23};  // every p by 200-apply A/B: r01_ab_orders_*.log
 const int kAutoVar1[9] = {D_, O_, O_, O_, O_, O_, O_, O_, O_};
-const int kAutoCfg1[9] = {0, 24, 31, 51, 40, 47, 47, 43, 45};  // p <= 2: r01_ab_orders_*.log; p >= 4: staged scatter, r02_ab_bp1_ys.log; p = 3: fused B-C-D, r02_ab_bcd_p3.log
+const int kAutoCfg1[9] = {0, 58, 58, 51, 40, 47, 47, 43, 45};  // p <= 2: thread per element, r02_ab_tpe.log; p = 3: fused B-C-D, r02_ab_bcd_p3.log; p >= 4: staged scatter, r02_ab_bp1_ys.log
 
 int auto_variant(int nc, int p, int q) {
   (void)q;

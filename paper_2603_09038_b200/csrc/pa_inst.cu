@@ -18,6 +18,7 @@
 #include "pa_dmma_warp.cuh"
 #include "pa_eo_bcd.cuh"
 #include "pa_eo_ds.cuh"
+#include "pa_eo_tpe.cuh"
 #include "pa_eo_dmmac.cuh"
 #include "pa_pipe.cuh"
 
@@ -77,6 +78,35 @@ void launch_warp_dmma(const OpView& v, const double* x, double* y, int blocks, c
   const StructIds sid = struct_ids(v);
   dmma_warp_kernel<D, Q, NC, W><<<blocks, 32 * W, WarpDmmaKernel<D, Q, NC, W>::SMEM, s>>>(
       tb, x, y, v.pa, v.ebits, v.nel, sid);
+}
+
+template <int D, int Q, int W>
+void launch_tpe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
+  FoldTables<D, Q> tb;
+  DfmaEoBody<D, Q, 1, 1, 32, EoLayDefault<D, Q, 1, false>>::fill(tb, v.B, v.G);
+  const StructIds sid = struct_ids(v);
+  tpe_kernel<D, Q, W><<<blocks, 32 * W, TpeLayout<D, Q, W>::SMEM, s>>>(tb, x, y, v.pa, v.ebits, v.nel, sid);
+}
+
+// thread-per-element BP1 (pa_eo_tpe.cuh): closed-form ids, 32 elements per warp
+template <int D, int Q, int W>
+KernelEntry tpe_entry(int cfg) {
+  KernelEntry k;
+  k.nc = 1;
+  k.d = D;
+  k.q = Q;
+  k.variant = FK_VARIANT_EO;
+  k.cfg = cfg;
+  k.E = 32 * W;
+  k.T = 32 * W;
+  k.persist = true;
+  k.structured = true;
+  k.smem = TpeLayout<D, Q, W>::SMEM;
+  k.func = reinterpret_cast<const void*>(&tpe_kernel<D, Q, W>);
+  k.launch = &launch_tpe<D, Q, W>;
+  k.diag = &launch_diag<D, Q, 1>;
+  k.diag_func = reinterpret_cast<const void*>(&diagonal_kernel<D, Q, 1>);
+  return k;
 }
 
 // warp-per-element DMMA (pa_dmma_warp.cuh): closed-form ids, D through L2
@@ -329,6 +359,12 @@ void add_all(std::vector<KernelEntry>& out) {
     out.push_back(entry<FK_VARIANT_EO, 55, D, Q, NC, S55, true, false, false, 1, true, true>());
     out.push_back(entry<FK_VARIANT_EO, 56, D, Q, NC, S56, true, false, false, 1, true, true>());
     out.push_back(entry<FK_VARIANT_EO, 57, D, Q, NC, S54, true, false, false, 1, true, false>());
+  }
+  // cfgs 58-59 (BP1, p <= 2): one thread per element, all stages in
+  // registers (pa_eo_tpe.cuh), 4 / 2 warps per CTA
+  if constexpr (NC == 1 && Q == D + 1 && D <= 3) {
+    out.push_back(tpe_entry<D, Q, 4>(58));
+    out.push_back(tpe_entry<D, Q, 2>(59));
   }
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;
