@@ -761,7 +761,7 @@ def run_sweep(a, peak):
 
     out = []
     cfgs = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(15)]
-            + [("eo", c) for c in range(60)] + [("mf", c) for c in range(11)])
+            + [("eo", c) for c in range(62)] + [("mf", c) for c in range(11)])
     if a.sweep_cfgs:
         want = set(a.sweep_cfgs.split(","))
         cfgs = [vc for vc in cfgs if f"{vc[0]}{vc[1]}" in want]

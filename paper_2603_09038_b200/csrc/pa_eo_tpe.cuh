@@ -38,8 +38,8 @@ struct TpeLayout {
   static constexpr size_t SMEM = 16ull * W + 8ull * W * WS;
 };
 
-template <int D, int Q, int W>
-__global__ void __launch_bounds__(32 * W) tpe_kernel(const __grid_constant__ FoldTables<D, Q> tb,
+template <int D, int Q, int W, int MINB = 1>
+__global__ void __launch_bounds__(32 * W, MINB) tpe_kernel(const __grid_constant__ FoldTables<D, Q> tb,
                                                      const double* __restrict__ x, double* __restrict__ y,
                                                      const double* __restrict__ pa,
                                                      const uint32_t* __restrict__ ebits, int nel,

@@ -80,16 +80,17 @@ void launch_warp_dmma(const OpView& v, const double* x, double* y, int blocks, c
       tb, x, y, v.pa, v.ebits, v.nel, sid);
 }
 
-template <int D, int Q, int W>
+template <int D, int Q, int W, int MINB>
 void launch_tpe(const OpView& v, const double* x, double* y, int blocks, cudaStream_t s) {
   FoldTables<D, Q> tb;
   DfmaEoBody<D, Q, 1, 1, 32, EoLayDefault<D, Q, 1, false>>::fill(tb, v.B, v.G);
   const StructIds sid = struct_ids(v);
-  tpe_kernel<D, Q, W><<<blocks, 32 * W, TpeLayout<D, Q, W>::SMEM, s>>>(tb, x, y, v.pa, v.ebits, v.nel, sid);
+  tpe_kernel<D, Q, W, MINB><<<blocks, 32 * W, TpeLayout<D, Q, W>::SMEM, s>>>(tb, x, y, v.pa, v.ebits, v.nel, sid);
 }
 
-// thread-per-element BP1 (pa_eo_tpe.cuh): closed-form ids, 32 elements per warp
-template <int D, int Q, int W>
+// thread-per-element BP1 (pa_eo_tpe.cuh): closed-form ids, 32 elements per
+// warp; MINB = CTAs per SM the register allocation must allow
+template <int D, int Q, int W, int MINB = 1>
 KernelEntry tpe_entry(int cfg) {
   KernelEntry k;
   k.nc = 1;
@@ -102,8 +103,8 @@ KernelEntry tpe_entry(int cfg) {
   k.persist = true;
   k.structured = true;
   k.smem = TpeLayout<D, Q, W>::SMEM;
-  k.func = reinterpret_cast<const void*>(&tpe_kernel<D, Q, W>);
-  k.launch = &launch_tpe<D, Q, W>;
+  k.func = reinterpret_cast<const void*>(&tpe_kernel<D, Q, W, MINB>);
+  k.launch = &launch_tpe<D, Q, W, MINB>;
   k.diag = &launch_diag<D, Q, 1>;
   k.diag_func = reinterpret_cast<const void*>(&diagonal_kernel<D, Q, 1>);
   return k;
@@ -360,11 +361,14 @@ void add_all(std::vector<KernelEntry>& out) {
     out.push_back(entry<FK_VARIANT_EO, 56, D, Q, NC, S56, true, false, false, 1, true, true>());
     out.push_back(entry<FK_VARIANT_EO, 57, D, Q, NC, S54, true, false, false, 1, true, false>());
   }
-  // cfgs 58-59 (BP1, p <= 2): one thread per element, all stages in
-  // registers (pa_eo_tpe.cuh), 4 / 2 warps per CTA
+  // cfgs 58-61 (BP1, p <= 2): one thread per element, all stages in
+  // registers (pa_eo_tpe.cuh), 4 / 2 warps per CTA; 60-61 with the register
+  // allocation capped for 3 / 6 CTAs per SM
   if constexpr (NC == 1 && Q == D + 1 && D <= 3) {
     out.push_back(tpe_entry<D, Q, 4>(58));
     out.push_back(tpe_entry<D, Q, 2>(59));
+    out.push_back(tpe_entry<D, Q, 4, 3>(60));  // registers capped for 3 CTAs (12 warps) per SM
+    out.push_back(tpe_entry<D, Q, 2, 6>(61));
   }
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;

@@ -118,7 +118,7 @@ def test_apply_matches_oracle_all_orders(variant, kind, p, qoff):
 
 
 LAUNCH_CONFIGS = ([("dfma", c) for c in range(7)] + [("dmma", c) for c in range(15)]
-                  + [("eo", c) for c in range(60)] + [("mf", c) for c in range(11)])
+                  + [("eo", c) for c in range(62)] + [("mf", c) for c in range(11)])
 
 
 @pytest.mark.parametrize("variant,cfg", LAUNCH_CONFIGS)
