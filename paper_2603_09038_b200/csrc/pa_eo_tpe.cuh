@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(32 * W, MINB) tpe_kernel(const __grid_constant
   using LY = TpeLayout<D, Q, W>;
   using G = GlobalLayout<D, Q, 1>;
   using Tab = FoldTables<D, Q>;
-  static_assert(D * D * D <= 32, "one Dirichlet word per element");
+  static_assert(D * D * D <= 64, "Dirichlet bits in one or two words");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int L = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + 2 * warp;
@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(32 * W, MINB) tpe_kernel(const __grid_constant
     const int ex = eg - eyz * sid.nx, ey = eyz - ez * sid.ny;
     const int base = ex * sid.p + sid.npx * (ey * sid.p + sid.npy * (ez * sid.p));
     const uint32_t bits = ebits ? ebits[(size_t)ee * G::MS] : 0u;
+    const uint32_t bits1 = (ebits && D * D * D > 32) ? ebits[(size_t)ee * G::MS + 1] : 0u;
     // ---- gather + stages A, B per z-plane k
     double t2[D][Q][Q];  // [k][b][a]: T2, then W in place
 #pragma unroll
@@ -93,7 +94,8 @@ __global__ void __launch_bounds__(32 * W, MINB) tpe_kernel(const __grid_constant
         for (int i = 0; i < D; ++i) {
           const int l = i + D * (j + D * k);
           const double v = x[base + i + sid.npx * (j + sid.npy * k)];
-          xr[i] = ((bits >> l) & 1u) ? 0.0 : v;
+          const uint32_t w = l < 32 ? bits : bits1;
+          xr[i] = ((w >> (l & 31)) & 1u) ? 0.0 : v;
         }
         contract_eo<D, Q, +1>(tab + Tab::TB, xr, t1[j]);
       }

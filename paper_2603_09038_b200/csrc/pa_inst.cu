@@ -370,6 +370,12 @@ void add_all(std::vector<KernelEntry>& out) {
     out.push_back(tpe_entry<D, Q, 4, 3>(60));  // registers capped for 3 CTAs (12 warps) per SM
     out.push_back(tpe_entry<D, Q, 2, 6>(61));
   }
+  // p = 3: T2 is 100 doubles per thread; 2 / 1 warps per CTA (33 KB of PA
+  // slots per warp)
+  if constexpr (NC == 1 && Q == D + 1 && D == 4) {
+    out.push_back(tpe_entry<D, Q, 2>(58));
+    out.push_back(tpe_entry<D, Q, 1>(59));
+  }
   // matrix-free (FK_VARIANT_MF): even-odd tuned bodies, D recomputed in stage C
   using M2 = TunedEo<D, Q, NC, E2, false, true>;
   using M1 = TunedEo<D, Q, NC, E1, false, true>;
