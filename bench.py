@@ -353,6 +353,10 @@ def init_ranks(a):
     shared = os.environ.get("FK_BENCH_DEVICE")
     if shared is not None:
         local = int(shared)
+    elif local >= torch.cuda.device_count():
+        raise SystemExit(f"--gpus {a.gpus}: rank {rank} needs cuda:{local} but {torch.cuda.device_count()} "
+                         f"GPU(s) are visible (one process per GPU; FK_BENCH_DEVICE=0 runs every rank on "
+                         f"cuda:0 to exercise the multi-rank path, not to measure scaling)")
     torch.cuda.set_device(local)
     if world == 1:
         return world, rank, local, None, None
