@@ -44,7 +44,7 @@ const std::vector<MixKernel>& mix_registry() {
   return reg;
 }
 
-const int kMixAutoCfg[9] = {0, 0, 0, 3, 2, 2, 0, 0, 4};  // order 8: staged outputs, r02_ab_bcd_p3.log
+const int kMixAutoCfg[9] = {0, 0, 8, 3, 10, 10, 8, 8, 4};  // single-X twins, r02_ab_mix_sx.log; order 8 staged outputs, r02_ab_bcd_p3.log
 
 int grid_for(int64_t n, int threads, int num_sms) {
   int64_t b = (n + threads - 1) / threads;

@@ -27,33 +27,34 @@ struct MixGeom {
   static constexpr int T = mix_round32(TL) > 384 ? 384 : mix_round32(TL);
 };
 
-// cfgs 4-7: the geometries of cfgs 0-3 with staged outputs (mix_pipe.cuh YS)
+// cfgs 4-7: the geometries of cfgs 0-3 with staged outputs (mix_pipe.cuh YS);
+// cfgs 8-11: the same geometries with one X buffer (SX); cfgs 12-15: both
 template <int DP, int DU, int Q, int CFG>
 void mix_launch(const MixKernel&, const double* Bp, const double* Gp, const double* Bu,
                 const double* w, double detj, const double* jinv, const MixArgs& a, int mode,
                 int blocks, cudaStream_t s) {
   using G = MixGeom<DP, DU, Q, CFG % 4>;
-  constexpr bool YS = CFG >= 4;
+  constexpr bool YS = CFG / 4 == 1 || CFG / 4 == 3, SX = CFG / 4 >= 2;
   MixTables<DP, DU, Q> tb;
   tb.fill(Bp, Gp, Bu);
   tb.fill_mf(w, detj, jinv);
-  const size_t smem = MixSmem<DP, DU, Q, G::E>::BYTES;
+  const size_t smem = MixSmem<DP, DU, Q, G::E, false, SX>::BYTES;
   if (mode == MIX_BOTH)
-    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, false, YS><<<blocks, G::T, smem, s>>>(tb, a);
+    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, false, YS, SX><<<blocks, G::T, smem, s>>>(tb, a);
   else if (mode == MIX_TAU)
-    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false, false, YS><<<blocks, G::T, smem, s>>>(tb, a);
+    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false, false, YS, SX><<<blocks, G::T, smem, s>>>(tb, a);
   else if (mode == MIX_VB)
-    mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true, false, YS><<<blocks, G::T, smem, s>>>(tb, a);
+    mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true, false, YS, SX><<<blocks, G::T, smem, s>>>(tb, a);
   else
-    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true, YS>
-        <<<blocks, G::T, MixSmem<DP, DU, Q, G::E, true>::BYTES, s>>>(tb, a);
+    mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true, YS, SX>
+        <<<blocks, G::T, MixSmem<DP, DU, Q, G::E, true, SX>::BYTES, s>>>(tb, a);
 }
 
 template <int P, int CFG>
 MixKernel mix_entry() {
   constexpr int DP = P + 1, DU = P, Q = P + 1;
   using G = MixGeom<DP, DU, Q, CFG % 4>;
-  constexpr bool YS = CFG >= 4;
+  constexpr bool YS = CFG / 4 == 1 || CFG / 4 == 3, SX = CFG / 4 >= 2;
   using L = MixLayout<DP, DU, Q>;
   MixKernel k;
   k.dp = DP;
@@ -64,12 +65,12 @@ MixKernel mix_entry() {
   k.T = G::T;
   k.ps = L::PS;
   k.gs = L::GS;
-  k.smem = MixSmem<DP, DU, Q, G::E>::BYTES;
-  k.smem_mf = MixSmem<DP, DU, Q, G::E, true>::BYTES;
-  k.f_both = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, false, YS>);
-  k.f_tau = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false, false, YS>);
-  k.f_vb = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true, false, YS>);
-  k.f_mf = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true, YS>);
+  k.smem = MixSmem<DP, DU, Q, G::E, false, SX>::BYTES;
+  k.smem_mf = MixSmem<DP, DU, Q, G::E, true, SX>::BYTES;
+  k.f_both = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, false, YS, SX>);
+  k.f_tau = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, false, false, YS, SX>);
+  k.f_vb = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, false, true, false, YS, SX>);
+  k.f_mf = reinterpret_cast<const void*>(&mix_pipe_kernel<DP, DU, Q, G::E, G::T, true, true, true, YS, SX>);
   k.launch = &mix_launch<DP, DU, Q, CFG>;
   return k;
 }
@@ -84,6 +85,14 @@ void mix_add(std::vector<MixKernel>& v) {
   v.push_back(mix_entry<P, 5>());
   v.push_back(mix_entry<P, 6>());
   v.push_back(mix_entry<P, 7>());
+  v.push_back(mix_entry<P, 8>());
+  v.push_back(mix_entry<P, 9>());
+  v.push_back(mix_entry<P, 10>());
+  v.push_back(mix_entry<P, 11>());
+  v.push_back(mix_entry<P, 12>());
+  v.push_back(mix_entry<P, 13>());
+  v.push_back(mix_entry<P, 14>());
+  v.push_back(mix_entry<P, 15>());
 }
 
 }  // namespace

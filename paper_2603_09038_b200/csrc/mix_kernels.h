@@ -25,7 +25,7 @@ struct MixKernel {
 };
 
 enum { MIX_BOTH = 0, MIX_TAU = 1, MIX_VB = 2, MIX_BOTH_MF = 3 };
-constexpr int kMixCfgs = 8;  // 0-3 geometries, 4-7 the same with staged outputs (YS)
+constexpr int kMixCfgs = 16;  // 0-3 geometries, 4-7 with staged outputs (YS), 8-11 with one X buffer (SX), 12-15 both
 
 constexpr int mix_round32(int n) { return (n + 31) / 32 * 32; }
 constexpr int cmax5(int a, int b, int c, int d, int e) {

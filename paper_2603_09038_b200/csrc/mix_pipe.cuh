@@ -158,8 +158,9 @@ struct MixLayout {
   static constexpr int GS = ((DP3 + 3) / 4) * 4;
 };
 
-template <int DP, int DU, int Q, int E, bool MF = false>
+template <int DP, int DU, int Q, int E, bool MF = false, bool SX = false>
 struct MixSmem {
+  static constexpr int NXB = SX ? 1 : 2;  // X buffers (SX: the next gather lands after stage A)
   using L = MixLayout<DP, DU, Q>;
   static constexpr size_t OFF_BAR = 0;  // 1 D barrier + 3 gid barriers
   static constexpr size_t OFF_DB = 32;
@@ -167,8 +168,8 @@ struct MixSmem {
   static constexpr size_t OFF_R0 = OFF_GS + 4ull * 3 * E * L::GS;
   static constexpr size_t OFF_R1 = OFF_R0 + 8ull * E * L::R0S;
   static constexpr size_t OFF_XP = OFF_R1 + 8ull * E * L::R1S;
-  static constexpr size_t OFF_XU = OFF_XP + 8ull * 2 * E * L::XPS;
-  static constexpr size_t BYTES = OFF_XU + 8ull * 2 * E * L::XUS;
+  static constexpr size_t OFF_XU = OFF_XP + 8ull * NXB * E * L::XPS;
+  static constexpr size_t BYTES = OFF_XU + 8ull * NXB * E * L::XUS;
 };
 
 struct MixArgs {
@@ -191,11 +192,16 @@ struct MixArgs {
 // contiguously across the batch's elements and out_p's RED.F64s go out in
 // node order — instead of one x-line per lane, where every warp-wide store /
 // RED touches ~32 rows (tools/scatter_bench.cu).
-template <int DP, int DU, int Q, int E, int T, bool TAU, bool VB, bool MF = false, bool YS = false>
+//
+// SX (single X buffer): the next batch's gather is issued after stage A has
+// consumed this batch's X instead of at the top of the batch — half the X
+// shared memory, so one more CTA fits per SM at order 4.
+template <int DP, int DU, int Q, int E, int T, bool TAU, bool VB, bool MF = false, bool YS = false,
+          bool SX = false>
 __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ MixTables<DP, DU, Q> tb,
                                                      const MixArgs arg) {
   using L = MixLayout<DP, DU, Q>;
-  using S = MixSmem<DP, DU, Q, E, MF>;
+  using S = MixSmem<DP, DU, Q, E, MF, SX>;
   using Tb = MixTables<DP, DU, Q>;
   constexpr int DP3 = L::DP3, DU3 = L::DU3, Q3 = L::Q3, GS = L::GS, PS = L::PS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -300,13 +306,15 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
     const int gslot = it % 3, h = it & 1;
     const int e0 = b * E, ne = min(E, nel - e0);
     const int nb = b + stride, nb2 = nb + stride;
-    const double* xp = xpb + h * E * L::XPS;
-    const double* xu = xub + h * E * L::XUS;
+    const double* xp = xpb + (SX ? 0 : h) * E * L::XPS;
+    const double* xu = xub + (SX ? 0 : h) * E * L::XUS;
     cp_async_wait_all();
     __syncthreads();
     if (nb < nbatch) {
-      wait_g((it + 1) % 3);
-      issue_x(nb, (it + 1) % 3, h ^ 1);
+      if constexpr (!SX) {
+        wait_g((it + 1) % 3);
+        issue_x(nb, (it + 1) % 3, h ^ 1);
+      }
       if (nb2 < nbatch && threadIdx.x == 0) {
         fence_proxy_async();
         issue_g(nb2, (it + 2) % 3);
@@ -336,6 +344,12 @@ __global__ void __launch_bounds__(T) mix_pipe_kernel(const __grid_constant__ Mix
       }
     });
     __syncthreads();
+    if constexpr (SX) {  // X(b) consumed: gather X(b+1) into the same buffer
+      if (nb < nbatch) {
+        wait_g((it + 1) % 3);
+        issue_x(nb, (it + 1) % 3, 0);
+      }
+    }
     // ---- stage B: y contraction
     lines(ne, NBP, NBU, [&](int e, int l) {
       if (TAU && l < NBP) {

@@ -153,13 +153,14 @@ def test_linear_pressure_gives_mass_weighted_unit_field():
     assert np.max(np.abs(r.u[1])) < 1e-13 and np.max(np.abs(r.u[2])) < 1e-13
 
 
-@pytest.mark.parametrize("cfg", range(8))
+@pytest.mark.parametrize("cfg", range(16))
 @pytest.mark.parametrize("strategy", ["FusedPA", "FusedMF"])
 @pytest.mark.parametrize("name", CASES)
 def test_every_mixed_launch_config(golden, name, strategy, cfg, monkeypatch):
-    """Every compiled geometry (FK_MIX_CFG, read at create): cfgs 0-3 and their
-    staged-output twins 4-7 (mix_pipe.cuh YS) — both blocks, the composed
-    normal operator (VB then TAU launches) and the matrix-free kernel."""
+    """Every compiled geometry (FK_MIX_CFG, read at create): cfgs 0-3, their
+    staged-output twins 4-7 (mix_pipe.cuh YS), single-X twins 8-11 (SX) and
+    both 12-15 — both blocks, the composed normal operator (VB then TAU
+    launches) and the matrix-free kernel."""
     from paper_2603_09038_b200 import MixedState
 
     monkeypatch.setenv("FK_MIX_CFG", str(cfg))
