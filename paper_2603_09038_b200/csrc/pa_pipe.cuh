@@ -154,6 +154,12 @@ struct PipeSmem {
 // GM = 1 (even-odd bodies): gather ids from the closed form (StructIds) —
 // no id array traffic, one int per element per slot.  SX: a single X buffer;
 // the next batch's gather is issued after stage A has consumed the current one.
+// XP: precomputed per-thread gather slots.  QF: the element quadratic form
+// twin (CG).  YS: staged scatter — stage E's outputs through the dead W
+// region, RED.F64s in node order.  DR (BP1, with DG): stage C's PA data loaded
+// into registers at the start of the batch.  Body traits FUSED_BCD
+// (pa_eo_bcd.cuh) and D_STREAM (pa_eo_ds.cuh) select the fused B-C-D stage
+// and the c-plane-pair ring of PA data.
 template <int D, int Q, int NC, class Body, bool PERSIST, bool DG = false, bool MF = false, int GM = 0,
           bool SX = false, bool XP = false, bool QF = false, bool YS = false, bool DR = false>
 __global__ void __launch_bounds__(Body::T) pa_pipe_kernel(const __grid_constant__ typename Body::Tab tb,
