@@ -486,6 +486,13 @@ int fk_mix_setup(fk_mix* m) {
   const int64_t nbatch = (m->nel + k.E - 1) / k.E;
   m->blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ * m->num_sms));
   m->blocks_mf = (int)std::max<int64_t>(1, std::min<int64_t>(nbatch, (int64_t)occ_mf * m->num_sms));
+  // test hook (as fk_api.cu): cap the persistent grid so small meshes run
+  // several batches per CTA (the cross-batch gather / id prefetches)
+  if (const char* c = std::getenv("FK_MAX_BLOCKS")) {
+    const int cap = std::max(1, std::atoi(c));
+    m->blocks = std::min(m->blocks, cap);
+    m->blocks_mf = std::min(m->blocks_mf, cap);
+  }
   for (auto& e : m->ev) FK_CUDA(cudaEventCreate(&e));
   m->is_setup = true;
   return FK_OK;

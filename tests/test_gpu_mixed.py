@@ -171,3 +171,20 @@ def test_every_mixed_launch_config(golden, name, strategy, cfg, monkeypatch):
     assert normwise(r.p, golden[f"{name}_FusedPA_out_p"]) <= TOL
     if strategy == "FusedPA":
         assert normwise(op.apply_fused_normal(u), golden[f"{name}_fused_normal"]) <= TOL
+
+
+@pytest.mark.parametrize("cfg", range(16))
+@pytest.mark.parametrize("name", ["m333_p6u5", "m443"])
+def test_every_mixed_launch_config_multi_batch(golden, name, cfg, monkeypatch):
+    """Persistent grid capped at 2 CTAs (FK_MAX_BLOCKS test hook): every CTA
+    walks several batches, so the cross-batch prefetches (gid slots, the
+    double or single X buffer, D after stage C) run, with a ragged last batch."""
+    from paper_2603_09038_b200 import MixedState
+
+    monkeypatch.setenv("FK_MIX_CFG", str(cfg))
+    monkeypatch.setenv("FK_MAX_BLOCKS", "2")
+    for strategy in ("FusedPA", "FusedMF"):
+        op = make(golden, name, strategy=strategy)
+        r = op.apply(MixedState(golden[f"{name}_u"], golden[f"{name}_p"]))
+        assert normwise(r.u, golden[f"{name}_FusedPA_out_u"]) <= TOL
+        assert normwise(r.p, golden[f"{name}_FusedPA_out_p"]) <= TOL

@@ -3,7 +3,7 @@ scatter (EO cfgs 40-49, incl. PA data in registers), stages B-D fused in
 registers (cfgs 50-53), the PA data streamed through a ring of c-plane pairs
 (cfgs 54-57, mbarrier ring with cross-batch prefetch: FK_MAX_BLOCKS=2 makes
 every CTA walk several batches) and the block operator's staged outputs
-(mixed cfgs 4-7).
+(mixed cfgs 4-7) and its single-X twins (mixed cfgs 8-15, several batches per CTA).
 
     compute-sanitizer --tool memcheck  python tools/sanitize_r02b.py
     compute-sanitizer --tool racecheck python tools/sanitize_r02b.py
@@ -37,10 +37,10 @@ for p, cfgs, kind in ((3, range(40, 54), "mass"), (4, range(40, 58), "diffusion"
                 continue
             finite(op.apply(torch.randn(op.num_dofs, dtype=torch.float64, device="cuda")))
             op.close()
-for cfg in range(4, 8):
+for cfg in range(4, 16):
     os.environ["FK_MIX_CFG"] = str(cfg)
     for p in (3, 4):
-        mop = MixedOperator(build_mesh(2, 3, 2), p, p - 1, p + 1)
+        mop = MixedOperator(build_mesh(4, 3, 3), p, p - 1, p + 1)
         s = MixedState(torch.randn(mop.u_shape, dtype=torch.float64, device="cuda"),
                        torch.randn(mop.num_p, dtype=torch.float64, device="cuda"))
         r = mop.apply(s)
